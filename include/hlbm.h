@@ -1,0 +1,126 @@
+/* hlbm.h -- C-ABI of the B200 HOME-LBM fluid step (libhlbm.so).
+ *
+ * Drop-in boundary for the reference package's solver path.  The reference
+ * (/root/reference/pkg/src/momentlbm) is pure Python and ships the step's arithmetic
+ * as NumPy array functions; its solver surface (SimGrid / SolverConfig / StepStats /
+ * fluid_update_step / run) is specified in SPEC.md:446-516 but not shipped.  The
+ * Python host layer (paper_2602_05295_b200.solver) binds these entry points with
+ * ctypes; INTEGRATION.md shows the binding.  Each entry point cites the reference
+ * interface it replaces.
+ *
+ * Conventions: plain pointers and sizes; the library owns all device memory; host
+ * arrays are caller-owned and copied.  Every call returns HLBM_OK (0) or an error code;
+ * hlbm_last_error() holds the message.  A context is driven by one host thread.
+ * Array layout = the reference's (moments.py:11-13): component axis first, then
+ * (x, y, z) in C order, float64; stress in Voigt order xx,xy,xz,yy,yz,zz (lattice.py:23).
+ */
+#ifndef HLBM_H
+#define HLBM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HLBM_OK 0
+#define HLBM_EINVAL 1      /* -> ValueError (moments.py:33-34; collision.py:102-103,203-204) */
+#define HLBM_EDIVERGED 2   /* -> FloatingPointError (collision.py:207-208)      */
+#define HLBM_ECUDA 3       /* -> RuntimeError                                               */
+
+#define HLBM_BC_PERIODIC 0
+#define HLBM_BC_INFLOW 1
+#define HLBM_BC_OUTFLOW 2
+#define HLBM_BC_WALL 3
+
+#define HLBM_FP32 0
+#define HLBM_Q16 1
+
+typedef struct hlbm_ctx hlbm_ctx;
+
+/* SolverConfig + SimGrid dims + QuantSpec. */
+typedef struct hlbm_config {
+  int32_t nx, ny, nz;          /* local interior dims of this slab (x is the slab axis)       */
+  int32_t gnx, gny, gnz;       /* global dims (== local on one GPU)                           */
+  int32_t x0;                  /* slab offset along x in the global grid                      */
+  int32_t x_lo_remote;         /* 1: x- ghost plane is filled by the caller (neighbour slab)  */
+  int32_t x_hi_remote;         /* 1: x+ ghost plane is filled by the caller                   */
+  double tau;                  /* relaxation time, tau = 0.5 + 3 nu (collision.py:30-31)      */
+  double force[3];             /* uniform body force (collision.py:137-194 `force`)           */
+  int32_t bc[6];               /* x-,x+,y-,y+,z-,z+ : HLBM_BC_*               */
+  double u_in[3];              /* inflow velocity                                             */
+  int32_t precision;           /* HLBM_FP32 or HLBM_Q16                                       */
+  double qmin[10], qmax[10];   /* codec ranges (rho, rho u_xyz, sneq xx..zz) */
+  int32_t bits[10];            /* bits per component, 8..16                 */
+  int32_t dither;              /* 1: counter-hash dither                         */
+  uint32_t seed;
+  int32_t device;              /* CUDA device ordinal                                         */
+  int32_t xseg;                /* interior-kernel x segment length (0 = default)              */
+} hlbm_config;
+
+/* StepStats. Sums run over fluid cells of this slab. */
+typedef struct hlbm_stats {
+  int64_t step;
+  double t_fluid_ms, t_copy_ms, t_solid_ms;
+  double mass;
+  double momentum[3];
+  double max_u;
+  int64_t saturation[10];
+  int64_t n_fluid;
+  int32_t finite;
+} hlbm_stats;
+
+const char* hlbm_version(void);
+
+/* SimGrid + SolverConfig construction.  Validates tau > 1/2
+ * (collision.py:102-103, 203-204) and the grid (nz % 4 == 0). */
+int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out);
+void hlbm_destroy(hlbm_ctx* ctx);
+const char* hlbm_last_error(const hlbm_ctx* ctx);
+
+/* Voxel solid mask, uint8 (nx,ny,nz) C order.  ghost_lo / ghost_hi: the (ny,nz) mask planes of
+ * the neighbouring slabs for remote faces (NULL: derived from the x BC).  Builds the sorted
+ * boundary-cell list and 27-bit link masks on the device (SPEC.md:400-402 SurfaceMask role). */
+int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, const uint8_t* ghost_hi);
+
+/* State in the reference layout: rho (nx,ny,nz), mom (3,nx,ny,nz), stress (6,nx,ny,nz) float64
+ * (moments.py:25-39 outputs; MomentSet fields moments.py:136-172). */
+int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const double* stress);
+int hlbm_get_moments(hlbm_ctx* ctx, double* rho, double* mom, double* stress);
+/* box [x0,x0+cx) x [y0,y0+cy) x [z0,z0+cz) of the slab interior (y, z wrap periodically) */
+int hlbm_get_moments_box(hlbm_ctx* ctx, int32_t x0, int32_t cx, int32_t y0, int32_t cy, int32_t z0,
+                         int32_t cz, double* rho, double* mom, double* stress);
+/* rho = rho0, u = sum_m a_m sin(2 pi k_m.x/N + phi_m), sneq = 0; modes: nmodes x 7 doubles */
+int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmodes);
+
+/* fluid_update_step x nsteps: interior kernel over every cell, then the
+ * compacted boundary/solid kernel; blocks until done and fills *out (may be NULL). Returns
+ * HLBM_EDIVERGED when max|u| >= 0.9 or a non-finite value appeared. */
+int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
+/* the same launches, enqueued on the context stream without synchronising */
+int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats);
+int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out);
+/* full-grid update with the per-cell pull kernel (GPU reference for the fast kernel) */
+int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps);
+
+/* boundary list: global linear cell indices (sorted) and link masks; cells==NULL -> count only */
+int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n);
+/* raw packed words of the q16 state, (5,nx,ny,nz) uint32 (SPEC.md:381 packed-buffer dump) */
+int hlbm_get_codes(hlbm_ctx* ctx, uint32_t* words);
+int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words);
+
+/* multi-GPU plumbing: run on an external stream (e.g. torch's), and expose the device planes
+ * that the x-slab halo exchange sends/receives for the CURRENT state buffer. */
+int hlbm_set_stream(hlbm_ctx* ctx, void* cuda_stream);
+int hlbm_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                     int64_t* bytes);
+/* device pointer of the current state buffer and its size (bytes) */
+int hlbm_state_buffer(hlbm_ctx* ctx, void** ptr, int64_t* bytes);
+int64_t hlbm_step_count(const hlbm_ctx* ctx);
+/* kernel launches issued by this context so far (evidence for the benchmark's launch count) */
+int64_t hlbm_launch_count(const hlbm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HLBM_H */

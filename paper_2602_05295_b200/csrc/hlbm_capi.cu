@@ -1,0 +1,577 @@
+// C-ABI implementation: context, buffers, stepping (host side of include/hlbm.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hlbm.h"
+#include "hlbm_launch.h"
+
+using namespace hlbm;
+
+struct hlbm_ctx {
+  hlbm_config cfg{};
+  int q16 = 0, NC = 10;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  size_t elem_bytes = 4;
+  int64_t plane_elems = 0, total_elems = 0;
+  void* buf[2] = {nullptr, nullptr};
+  int cur = 0;
+  Stats* d_stats = nullptr;
+  Relax R{};
+  Codec Q{};
+  Ranges RG{};
+  float inflow[10] = {};
+  int x_lo_src = 0, x_hi_src = 0;
+  // solids
+  int64_t* d_bcells = nullptr;
+  uint32_t* d_bmasks = nullptr;
+  int64_t nb = 0;
+  int64_t* d_scells = nullptr;
+  int64_t ns = 0;
+  uint32_t* d_bits = nullptr;
+  int bits_row_words = 0;
+  int64_t steps = 0;
+  int64_t launches = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  double last_t_fluid = 0, last_t_solid = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(hlbm_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(ctx, HLBM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+Geo make_geo(const hlbm_ctx* ctx) {
+  const hlbm_config& c = ctx->cfg;
+  Geo g{};
+  g.nx = c.nx; g.ny = c.ny; g.nz = c.nz;
+  g.cstride = (int64_t)c.ny * c.nz;
+  g.pstride = ctx->plane_elems;
+  g.x_lo_src = ctx->x_lo_src;
+  g.x_hi_src = ctx->x_hi_src;
+  g.nzt = (c.nz + kZT - 1) / kZT;
+  g.nyt = (c.ny + kRows - 1) / kRows;
+  g.xseg = c.xseg > 0 ? c.xseg : 64;
+  if (g.xseg > c.nx) g.xseg = c.nx;
+  g.nxs = (c.nx + g.xseg - 1) / g.xseg;
+  g.gx0 = c.x0; g.gny = c.gny; g.gnz = c.gnz; g.gnx_total = c.gnx;
+  return g;
+}
+
+uint32_t step_key(int64_t step, uint32_t seed) {   // oracle/codec.py: step_key
+  const uint64_t v = ((uint64_t)step * 0x9E3779B9ull + (uint64_t)seed * 0x85EBCA6Bull + 0x2545F491ull) &
+                     0xFFFFFFFFull;
+  return mix32((uint32_t)v);
+}
+
+StepArgs make_args(hlbm_ctx* ctx, int with_stats) {
+  StepArgs A{};
+  A.in = ctx->buf[ctx->cur];
+  A.out = ctx->buf[1 - ctx->cur];
+  A.g = make_geo(ctx);
+  A.R = ctx->R;
+  A.Q = ctx->Q;
+  for (int i = 0; i < 10; ++i) A.inflow[i] = ctx->inflow[i];
+  A.special_bits = ctx->d_bits;
+  A.bits_row_words = ctx->bits_row_words;
+  A.step_key = step_key(ctx->steps, ctx->cfg.seed);
+  A.do_stats = with_stats;
+  A.stats = ctx->d_stats;
+  return A;
+}
+
+unsigned long long* sat_ptr(hlbm_ctx* ctx) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->d_stats) + offsetof(Stats, sat));
+}
+
+bool has_force(const hlbm_ctx* ctx) {
+  return ctx->cfg.force[0] != 0.0 || ctx->cfg.force[1] != 0.0 || ctx->cfg.force[2] != 0.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hlbm_version(void) { return "hlbm-b200 0.1 (sm_100a)"; }
+
+const char* hlbm_last_error(const hlbm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
+  if (!cfg || !out) return HLBM_EINVAL;
+  *out = nullptr;
+  hlbm_ctx* ctx = new hlbm_ctx();
+  ctx->cfg = *cfg;
+  hlbm_config& c = ctx->cfg;
+  auto bad = [&](const std::string& m) {
+    int r = fail(ctx, HLBM_EINVAL, m);
+    *out = ctx;   // caller reads the message, then destroys
+    return r;
+  };
+  if (c.nx < 1 || c.ny < 1 || c.nz < 4) return bad("grid dims must be >= 1 (nz >= 4)");
+  if (c.nz % 4 != 0) return bad("nz must be a multiple of 4");
+  if (c.gnx <= 0) c.gnx = c.nx;
+  if (c.gny <= 0) c.gny = c.ny;
+  if (c.gnz <= 0) c.gnz = c.nz;
+  if (c.gny != c.ny || c.gnz != c.nz) return bad("slabs split x only: gny/gnz must equal ny/nz");
+  if ((int64_t)c.gnx * c.gny * c.gnz >= (int64_t)1 << 32) return bad("global grid exceeds 2^32 cells");
+  if (!(c.tau > 0.5)) return bad("tau must exceed 0.5 (non-negative viscosity)");
+  for (int f = 0; f < 6; ++f)
+    if (c.bc[f] < 0 || c.bc[f] > 3) return bad("unknown boundary condition");
+  for (int f = 2; f < 6; ++f)
+    if (c.bc[f] == HLBM_BC_INFLOW || c.bc[f] == HLBM_BC_OUTFLOW)
+      return bad("y/z faces support periodic or wall only");
+  if ((c.bc[0] == HLBM_BC_PERIODIC) != (c.bc[1] == HLBM_BC_PERIODIC) && !(c.x_lo_remote || c.x_hi_remote))
+    return bad("periodic x needs both x faces periodic");
+  if ((c.bc[2] == HLBM_BC_PERIODIC) != (c.bc[3] == HLBM_BC_PERIODIC) ||
+      (c.bc[4] == HLBM_BC_PERIODIC) != (c.bc[5] == HLBM_BC_PERIODIC))
+    return bad("periodic y/z needs both faces periodic");
+  if (c.precision != HLBM_FP32 && c.precision != HLBM_Q16) return bad("unknown precision");
+  ctx->q16 = c.precision == HLBM_Q16;
+  ctx->NC = ctx->q16 ? 5 : 10;
+  if (ctx->q16) {
+    for (int k = 0; k < 10; ++k) {
+      if (c.bits[k] == 0) c.bits[k] = 16;
+      if (c.bits[k] < 2 || c.bits[k] > 16) return bad("bits per component must lie in [2, 16]");
+      if (!(c.qmax[k] > c.qmin[k])) return bad("quantization range needs min < max");
+    }
+  }
+  if (cudaSetDevice(c.device) != cudaSuccess) return bad("cannot select CUDA device");
+
+  // relaxation constants (collision.py:158-191)
+  const double tau = c.tau, s = 1.0 / tau;
+  ctx->R.om = (float)(1.0 - s);
+  ctx->R.cxy = (float)((2 * tau - 1) / (2 * tau));
+  ctx->R.cd = (float)((tau - 1) / (3 * tau));
+  ctx->R.fx = (float)c.force[0];
+  ctx->R.fy = (float)c.force[1];
+  ctx->R.fz = (float)c.force[2];
+  // inflow ghost state: rho = 1, j = u_in, sneq = 0
+  for (int k = 0; k < 10; ++k) ctx->inflow[k] = 0.f;
+  ctx->inflow[1] = (float)c.u_in[0];
+  ctx->inflow[2] = (float)c.u_in[1];
+  ctx->inflow[3] = (float)c.u_in[2];
+  // codec
+  for (int k = 0; k < 10; ++k) {
+    const double mn = ctx->q16 ? c.qmin[k] : 0.0, mx = ctx->q16 ? c.qmax[k] : 1.0;
+    const double L = ctx->q16 ? (double)((1u << c.bits[k]) - 1u) : 1.0;
+    ctx->RG.mn[k] = mn;
+    ctx->RG.mx[k] = mx;
+    ctx->RG.levels[k] = L;
+    const double shift = (k == 0) ? 1.0 : 0.0;   // component 0 is held as d = rho - 1
+    ctx->Q.dec_step[k] = (float)((mx - mn) / L);
+    ctx->Q.dec_off[k] = (float)(mn - shift);
+    const double sc = L / (mx - mn);
+    ctx->Q.enc_scale[k] = (float)sc;
+    ctx->Q.enc_off[k] = (float)((shift - mn) * sc + 0.5);
+    const double mid = 0.5 * (mn + mx), half = 0.5 * (mx - mn);
+    ctx->Q.sat_a[k] = (float)(1.0 / half);
+    ctx->Q.sat_b[k] = (float)((shift - mid) / half);
+    ctx->Q.levels[k] = (uint32_t)L;
+  }
+  // source-plane map for x = -1 / x = nx
+  const int nx = c.nx;
+  if (c.x_lo_remote) ctx->x_lo_src = 0;
+  else if (c.bc[0] == HLBM_BC_PERIODIC) ctx->x_lo_src = nx;
+  else if (c.bc[0] == HLBM_BC_INFLOW) ctx->x_lo_src = -1;
+  else ctx->x_lo_src = 1;   // outflow: zero-gradient copy; wall: links bounce back
+  if (c.x_hi_remote) ctx->x_hi_src = nx + 1;
+  else if (c.bc[1] == HLBM_BC_PERIODIC) ctx->x_hi_src = 1;
+  else if (c.bc[1] == HLBM_BC_INFLOW) ctx->x_hi_src = -1;
+  else ctx->x_hi_src = nx;
+
+  ctx->elem_bytes = 4;
+  ctx->plane_elems = (int64_t)ctx->NC * c.ny * c.nz;
+  ctx->total_elems = ctx->plane_elems * (nx + 2);
+  *out = ctx;
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  ctx->own_stream = true;
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaMalloc(&ctx->buf[b], ctx->total_elems * 4));
+    CK(cudaMemset(ctx->buf[b], 0, ctx->total_elems * 4));
+  }
+  CK(cudaMalloc(&ctx->d_stats, sizeof(Stats)));
+  CK(cudaMemset(ctx->d_stats, 0, sizeof(Stats)));
+  for (int i = 0; i < 3; ++i) CK(cudaEventCreate(&ctx->ev[i]));
+  // default state: rest (rho = 1, j = 0, sneq = 0) in both buffers
+  for (int b = 0; b < 2; ++b)
+    CK(launch_init_modes(make_geo(ctx), ctx->q16, ctx->RG, ctx->buf[b], 1.0, nullptr, 0, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HLBM_OK;
+}
+
+void hlbm_destroy(hlbm_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (int b = 0; b < 2; ++b) cudaFree(ctx->buf[b]);
+  cudaFree(ctx->d_stats);
+  cudaFree(ctx->d_bcells);
+  cudaFree(ctx->d_bmasks);
+  cudaFree(ctx->d_scells);
+  cudaFree(ctx->d_bits);
+  for (int i = 0; i < 3; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int hlbm_set_stream(hlbm_ctx* ctx, void* stream) {
+  if (!ctx) return HLBM_EINVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = (cudaStream_t)stream;
+  ctx->own_stream = false;
+  return HLBM_OK;
+}
+
+int64_t hlbm_step_count(const hlbm_ctx* ctx) { return ctx ? ctx->steps : -1; }
+int64_t hlbm_launch_count(const hlbm_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int hlbm_state_buffer(hlbm_ctx* ctx, void** ptr, int64_t* bytes) {
+  if (!ctx) return HLBM_EINVAL;
+  if (ptr) *ptr = ctx->buf[ctx->cur];
+  if (bytes) *bytes = ctx->total_elems * 4;
+  return HLBM_OK;
+}
+
+int hlbm_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                     int64_t* bytes) {
+  if (!ctx) return HLBM_EINVAL;
+  char* b = (char*)ctx->buf[ctx->cur];
+  const int64_t pb = ctx->plane_elems * 4;
+  if (send_lo) *send_lo = b + 1 * pb;
+  if (send_hi) *send_hi = b + (int64_t)ctx->cfg.nx * pb;
+  if (recv_lo) *recv_lo = b;
+  if (recv_hi) *recv_hi = b + (int64_t)(ctx->cfg.nx + 1) * pb;
+  if (bytes) *bytes = pb;
+  return HLBM_OK;
+}
+
+int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const double* stress) {
+  if (!ctx || !rho || !mom || !stress) return fail(ctx, HLBM_EINVAL, "null argument");
+  const hlbm_config& c = ctx->cfg;
+  const int64_t n = (int64_t)c.nx * c.ny * c.nz;
+  for (int64_t i = 0; i < n; ++i)
+    if (!(rho[i] > 0.0)) return fail(ctx, HLBM_EINVAL, "density must be positive");   // moments.py:147
+  const int64_t pl = (int64_t)c.ny * c.nz;
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(c.nx, (64ll << 20) / (pl * 80)));
+  double *dr, *dm, *ds;
+  CK(cudaMalloc(&dr, chunk * pl * 8));
+  CK(cudaMalloc(&dm, 3 * chunk * pl * 8));
+  CK(cudaMalloc(&ds, 6 * chunk * pl * 8));
+  CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+  const Geo g = make_geo(ctx);
+  for (int x0 = 0; x0 < c.nx; x0 += chunk) {
+    const int cnt = std::min(chunk, c.nx - x0);
+    const int64_t m = cnt * pl;
+    CK(cudaMemcpyAsync(dr, rho + x0 * pl, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (int k = 0; k < 3; ++k)
+      CK(cudaMemcpyAsync(dm + k * m, mom + k * n + x0 * pl, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (int k = 0; k < 6; ++k)
+      CK(cudaMemcpyAsync(ds + k * m, stress + k * n + x0 * pl, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_import(g, ctx->RG, ctx->q16, ctx->buf[ctx->cur], dr, dm, ds, x0, cnt,
+                     sat_ptr(ctx), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(dr);
+  cudaFree(dm);
+  cudaFree(ds);
+  return HLBM_OK;
+}
+
+int hlbm_get_moments_box(hlbm_ctx* ctx, int32_t x0, int32_t cx, int32_t y0, int32_t cy, int32_t z0,
+                         int32_t cz, double* rho, double* mom, double* stress) {
+  if (!ctx || !rho || !mom || !stress) return fail(ctx, HLBM_EINVAL, "null argument");
+  const hlbm_config& c = ctx->cfg;
+  if (x0 < 0 || cx < 0 || x0 + cx > c.nx || cy < 0 || cz < 0) return fail(ctx, HLBM_EINVAL, "box out of range");
+  const int64_t pl = (int64_t)cy * cz;
+  if (pl == 0 || cx == 0) return HLBM_OK;
+  const int64_t n = pl * cx;
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(cx, (64ll << 20) / (pl * 80)));
+  double *dr, *dm, *ds;
+  CK(cudaMalloc(&dr, chunk * pl * 8));
+  CK(cudaMalloc(&dm, 3 * chunk * pl * 8));
+  CK(cudaMalloc(&ds, 6 * chunk * pl * 8));
+  const Geo g = make_geo(ctx);
+  for (int xa = 0; xa < cx; xa += chunk) {
+    const int cnt = std::min(chunk, cx - xa);
+    const int64_t m = cnt * pl;
+    CK(launch_export(g, ctx->RG, ctx->q16, ctx->buf[ctx->cur], dr, dm, ds, x0 + xa, cnt, y0, cy, z0, cz,
+                     ctx->stream));
+    CK(cudaMemcpyAsync(rho + xa * pl, dr, m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    for (int k = 0; k < 3; ++k)
+      CK(cudaMemcpyAsync(mom + k * n + xa * pl, dm + k * m, m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    for (int k = 0; k < 6; ++k)
+      CK(cudaMemcpyAsync(stress + k * n + xa * pl, ds + k * m, m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(dr);
+  cudaFree(dm);
+  cudaFree(ds);
+  return HLBM_OK;
+}
+
+int hlbm_get_moments(hlbm_ctx* ctx, double* rho, double* mom, double* stress) {
+  if (!ctx) return HLBM_EINVAL;
+  return hlbm_get_moments_box(ctx, 0, ctx->cfg.nx, 0, ctx->cfg.ny, 0, ctx->cfg.nz, rho, mom, stress);
+}
+
+int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmodes) {
+  if (!ctx || (nmodes > 0 && !modes) || nmodes < 0) return fail(ctx, HLBM_EINVAL, "bad modes");
+  if (!(rho0 > 0.0)) return fail(ctx, HLBM_EINVAL, "density must be positive");
+  double* dmodes = nullptr;
+  if (nmodes > 0) {
+    CK(cudaMalloc(&dmodes, (size_t)nmodes * 7 * 8));
+    CK(cudaMemcpy(dmodes, modes, (size_t)nmodes * 7 * 8, cudaMemcpyHostToDevice));
+  }
+  CK(launch_init_modes(make_geo(ctx), ctx->q16, ctx->RG, ctx->buf[ctx->cur], rho0, dmodes, nmodes,
+                       ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(dmodes);
+  return HLBM_OK;
+}
+
+int hlbm_get_codes(hlbm_ctx* ctx, uint32_t* words) {
+  if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
+  if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
+  const hlbm_config& c = ctx->cfg;
+  const int64_t pl = (int64_t)c.ny * c.nz, n = pl * c.nx;
+  // device [x][k][y][z] -> host [k][x][y][z]
+  CK(cudaMemcpy2DAsync(words, pl * 4, (char*)ctx->buf[ctx->cur] + ctx->plane_elems * 4, ctx->plane_elems * 4,
+                       pl * 4, c.nx, cudaMemcpyDeviceToHost, ctx->stream));
+  for (int k = 1; k < 5; ++k)
+    CK(cudaMemcpy2DAsync(words + k * n, pl * 4,
+                         (char*)ctx->buf[ctx->cur] + ctx->plane_elems * 4 + k * pl * 4,
+                         ctx->plane_elems * 4, pl * 4, c.nx, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HLBM_OK;
+}
+
+int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words) {
+  if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
+  if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
+  const hlbm_config& c = ctx->cfg;
+  const int64_t pl = (int64_t)c.ny * c.nz, n = pl * c.nx;
+  for (int k = 0; k < 5; ++k)
+    CK(cudaMemcpy2DAsync((char*)ctx->buf[ctx->cur] + ctx->plane_elems * 4 + k * pl * 4, ctx->plane_elems * 4,
+                         words + k * n, pl * 4, pl * 4, c.nx, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HLBM_OK;
+}
+
+int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, const uint8_t* ghost_hi) {
+  if (!ctx || !mask) return fail(ctx, HLBM_EINVAL, "null mask");
+  const hlbm_config& c = ctx->cfg;
+  const int64_t pl = (int64_t)c.ny * c.nz, n = pl * c.nx;
+  // planes -1 .. nx of the padded mask along x (oracle/step.py:padded_solid)
+  std::vector<uint8_t> ext((size_t)(n + 2 * pl));
+  for (int64_t i = 0; i < n; ++i) ext[pl + i] = mask[i] ? 1 : 0;
+  auto fill_ghost = [&](uint8_t* dst, const uint8_t* remote, int bc, bool lo) {
+    if (remote) {
+      for (int64_t i = 0; i < pl; ++i) dst[i] = remote[i] ? 1 : 0;
+    } else if (bc == HLBM_BC_PERIODIC) {
+      const uint8_t* src = ext.data() + pl + (lo ? (int64_t)(c.nx - 1) * pl : 0);
+      memcpy(dst, src, pl);
+    } else {
+      memset(dst, bc == HLBM_BC_WALL ? 1 : 0, pl);
+    }
+  };
+  fill_ghost(ext.data(), c.x_lo_remote ? ghost_lo : nullptr, c.bc[0], true);
+  fill_ghost(ext.data() + pl + n, c.x_hi_remote ? ghost_hi : nullptr, c.bc[1], false);
+  if ((c.x_lo_remote && !ghost_lo) || (c.x_hi_remote && !ghost_hi))
+    return fail(ctx, HLBM_EINVAL, "remote x faces need the neighbour's ghost mask plane");
+
+  cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
+  cudaFree(ctx->d_bmasks); ctx->d_bmasks = nullptr;
+  cudaFree(ctx->d_scells); ctx->d_scells = nullptr;
+  cudaFree(ctx->d_bits); ctx->d_bits = nullptr;
+  ctx->nb = ctx->ns = 0;
+
+  uint8_t *d_ext, *d_cls;
+  uint32_t* d_links;
+  int64_t *d_counts, *d_total;
+  const int64_t nt = compact_tiles(n);
+  CK(cudaMalloc(&d_ext, ext.size()));
+  CK(cudaMalloc(&d_cls, n));
+  CK(cudaMalloc(&d_links, n * 4));
+  CK(cudaMalloc(&d_counts, (nt + 1) * 8));
+  CK(cudaMalloc(&d_total, 8));
+  CK(cudaMemcpy(d_ext, ext.data(), ext.size(), cudaMemcpyHostToDevice));
+  MaskGeo mg{c.nx, c.ny, c.nz, c.bc[2] == HLBM_BC_WALL, c.bc[3] == HLBM_BC_WALL, c.bc[4] == HLBM_BC_WALL,
+             c.bc[5] == HLBM_BC_WALL};
+  CK(launch_classify(d_ext, mg, d_links, d_cls, ctx->stream));
+  for (int pass = 0; pass < 2; ++pass) {
+    const uint8_t want = pass == 0 ? 1 : 2;
+    CK(launch_compact(d_cls, d_links, n, want, d_counts, d_total, nullptr, nullptr, true, ctx->stream));
+    int64_t tot = 0;
+    CK(cudaMemcpyAsync(&tot, d_total, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (tot > 0) {
+      int64_t* cells;
+      uint32_t* masks = nullptr;
+      CK(cudaMalloc(&cells, tot * 8));
+      if (pass == 0) CK(cudaMalloc(&masks, tot * 4));
+      CK(launch_compact(d_cls, d_links, n, want, d_counts, d_total, cells, masks, false, ctx->stream));
+      if (pass == 0) { ctx->d_bcells = cells; ctx->d_bmasks = masks; ctx->nb = tot; }
+      else { ctx->d_scells = cells; ctx->ns = tot; }
+    }
+  }
+  if (ctx->nb + ctx->ns > 0) {
+    ctx->bits_row_words = (c.nz + 31) / 32;
+    CK(cudaMalloc(&ctx->d_bits, (int64_t)c.nx * c.ny * ctx->bits_row_words * 4));
+    CK(launch_special_bits(d_cls, c.nx, c.ny, c.nz, ctx->bits_row_words, ctx->d_bits, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_ext);
+  cudaFree(d_cls);
+  cudaFree(d_links);
+  cudaFree(d_counts);
+  cudaFree(d_total);
+  return HLBM_OK;
+}
+
+int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n) {
+  if (!ctx || !n) return fail(ctx, HLBM_EINVAL, "null argument");
+  if (!cells) { *n = ctx->nb; return HLBM_OK; }
+  if (*n < ctx->nb) return fail(ctx, HLBM_EINVAL, "output buffer too small");
+  *n = ctx->nb;
+  if (ctx->nb == 0) return HLBM_OK;
+  CK(cudaMemcpy(cells, ctx->d_bcells, ctx->nb * 8, cudaMemcpyDeviceToHost));
+  if (masks) CK(cudaMemcpy(masks, ctx->d_bmasks, ctx->nb * 4, cudaMemcpyDeviceToHost));
+  // local -> global linear index
+  const int64_t off = (int64_t)ctx->cfg.x0 * ctx->cfg.ny * ctx->cfg.nz;
+  for (int64_t i = 0; i < ctx->nb; ++i) cells[i] += off;
+  return HLBM_OK;
+}
+
+int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
+  if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
+  const bool special = ctx->nb + ctx->ns > 0;
+  for (int s = 0; s < nsteps; ++s) {
+    const int st = (with_stats && s == nsteps - 1) ? 1 : 0;
+    if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+    StepArgs A = make_args(ctx, st);
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->stream));
+    ++ctx->launches;
+    if (ctx->nb) {
+      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    if (ctx->ns) {
+      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    ctx->cur = 1 - ctx->cur;
+    ++ctx->steps;
+  }
+  return HLBM_OK;
+}
+
+int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
+  if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
+  const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
+  for (int s = 0; s < nsteps; ++s) {
+    StepArgs A = make_args(ctx, 0);
+    CK(launch_pull_cells(A, nullptr, nullptr, n, 0, q16, force, dither, ctx->stream));
+    ++ctx->launches;
+    if (ctx->nb) {
+      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    if (ctx->ns) {
+      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    ctx->cur = 1 - ctx->cur;
+    ++ctx->steps;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HLBM_OK;
+}
+
+int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {
+  if (!ctx) return HLBM_EINVAL;
+  Stats h{};
+  CK(cudaMemcpyAsync(&h, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const hlbm_config& c = ctx->cfg;
+  const int64_t nfluid = (int64_t)c.nx * c.ny * c.nz - ctx->ns;
+  float mu2;
+  memcpy(&mu2, &h.max_u2_bits, 4);
+  hlbm_stats s{};
+  s.step = ctx->steps;
+  s.t_fluid_ms = ctx->last_t_fluid;
+  s.t_copy_ms = 0.0;
+  s.t_solid_ms = ctx->last_t_solid;
+  s.mass = (double)nfluid + h.mass_dev;
+  for (int k = 0; k < 3; ++k) s.momentum[k] = h.mom[k];
+  s.max_u = std::sqrt((double)mu2);
+  for (int k = 0; k < 10; ++k) s.saturation[k] = (int64_t)h.sat[k];
+  s.n_fluid = nfluid;
+  s.finite = std::isfinite(s.mass) && std::isfinite(s.momentum[0]) && std::isfinite(s.momentum[1]) &&
+             std::isfinite(s.momentum[2]) && std::isfinite(s.max_u);
+  if (out) *out = s;
+  if (!s.finite) return fail(ctx, HLBM_EDIVERGED, "non-finite moment detected (solver divergence)");
+  if (s.max_u >= 0.9) return fail(ctx, HLBM_EDIVERGED, "max |u| reached 0.9 (solver divergence)");
+  return HLBM_OK;
+}
+
+int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
+  if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  if (nsteps == 0) {
+    if (out) { memset(out, 0, sizeof(*out)); out->step = ctx->steps; out->finite = 1; }
+    return HLBM_OK;
+  }
+  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
+  const bool special = ctx->nb + ctx->ns > 0;
+  double tf = 0, ts = 0;
+  for (int s = 0; s < nsteps; ++s) {
+    const int st = (s == nsteps - 1) ? 1 : 0;
+    if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+    StepArgs A = make_args(ctx, st);
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->stream));
+    ++ctx->launches;
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    if (ctx->nb) {
+      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    if (ctx->ns) {
+      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    CK(cudaEventSynchronize(ctx->ev[2]));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+    tf += a;
+    ts += b;
+    ctx->cur = 1 - ctx->cur;
+    ++ctx->steps;
+  }
+  ctx->last_t_fluid = tf / nsteps;
+  ctx->last_t_solid = ts / nsteps;
+  return hlbm_read_stats(ctx, out);
+}
+
+}  // extern "C"

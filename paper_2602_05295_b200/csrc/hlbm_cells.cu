@@ -1,0 +1,552 @@
+// Compacted per-cell kernels (split scheme, §4.2 / Alg. 3 role):
+//
+//   pull_cells      one thread per listed cell: full pull update over the 27 links, with every
+//                   link whose source x - c_i is solid replaced by half-way bounce-back
+//                   f_i(x) <- f+_opp(i)(x) (opposite table lattice.py:198-201).
+//                   Run over the boundary-cell list after fluid_interior; with no list and
+//                   zero masks it is also the full-grid GPU reference update.
+//   reset_solid     solid cells -> rest state (they never feed a fluid cell: every link out of
+//                   a solid cell is cut and bounced back).
+//   classify / compact   voxel mask -> sorted boundary-cell list + 27-bit link masks and the
+//                   solid list, deterministic (block prefix sums, no atomics in the ordering).
+//   import / export reference layout (rho, mom, stress float64) <-> internal state.
+#include "hlbm_launch.h"
+
+namespace hlbm {
+
+// D3Q27 order of lattice.py:99-116
+__device__ constexpr int kCX[27] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1};
+__device__ constexpr int kCY[27] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, -1, 1, -1, 1};
+__device__ constexpr int kCZ[27] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, -1, 1};
+
+__device__ __forceinline__ int src_plane(const Geo& g, int x) {   // storage plane of source x
+  if (x < 0) return g.x_lo_src;
+  if (x >= g.nx) return g.x_hi_src;
+  return x + 1;
+}
+
+template <bool Q16>
+__device__ __forceinline__ void load_cell(const StepArgs& A, int sp, int y, int z, float s[10]) {
+  const Geo& g = A.g;
+  if (sp < 0) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s[c] = A.inflow[c];
+    return;
+  }
+  const int64_t off = (int64_t)sp * g.pstride + (int64_t)y * g.nz + z;
+  if (!Q16) {
+    const float* p = reinterpret_cast<const float*>(A.in) + off;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s[c] = __ldg(p + c * g.cstride);
+  } else {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(A.in) + off;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t wv = __ldg(p + k * g.cstride);
+      s[2 * k] = __fmaf_rn(code_lo_f(wv) - 8388608.0f, A.Q.dec_step[2 * k], A.Q.dec_off[2 * k]);
+      s[2 * k + 1] = __fmaf_rn(code_hi_f(wv) - 8388608.0f, A.Q.dec_step[2 * k + 1], A.Q.dec_off[2 * k + 1]);
+    }
+  }
+}
+
+// one link of the pull update; accumulates the raw moments of ft into m
+template <int I, bool Q16, bool FORCE>
+__device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z, uint32_t mask,
+                                          float m[10]) {
+  constexpr int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
+  const Geo& g = A.g;
+  const bool bb = (mask >> I) & 1u;
+  const int sx = bb ? x : x - cx;
+  const int sy = bb ? y : wrapi(y - cy, g.ny);
+  const int sz = bb ? z : wrapi(z - cz, g.nz);
+  float s[10];
+  load_cell<Q16>(A, src_plane(g, sx), sy, sz, s);
+  const Coef<float> C = coeffs<float, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+  float E, O;
+  eval_eo<cx, cy, cz, float>(C, E, O);
+  const float ft = bb ? (E - O) : (E + O);
+  m[0] += ft;
+  if (cx) m[1] += cx * ft;
+  if (cy) m[2] += cy * ft;
+  if (cz) m[3] += cz * ft;
+  if (cx) m[4] += ft;
+  if (cx && cy) m[5] += cx * cy * ft;
+  if (cx && cz) m[6] += cx * cz * ft;
+  if (cy) m[7] += ft;
+  if (cy && cz) m[8] += cy * cz * ft;
+  if (cz) m[9] += ft;
+}
+
+template <int I, bool Q16, bool FORCE>
+struct PullAll {
+  __device__ __forceinline__ static void run(const StepArgs& A, int x, int y, int z, uint32_t mask,
+                                             float m[10]) {
+    pull_link<I, Q16, FORCE>(A, x, y, z, mask, m);
+    PullAll<I + 1, Q16, FORCE>::run(A, x, y, z, mask, m);
+  }
+};
+template <bool Q16, bool FORCE>
+struct PullAll<27, Q16, FORCE> {
+  __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*) {}
+};
+
+template <bool Q16, bool DITHER>
+__device__ __forceinline__ void store_cell(const StepArgs& A, int x, int y, int z, const float s[10],
+                                           bool stat, float red[5]) {
+  const Geo& g = A.g;
+  const int64_t off = (int64_t)(x + 1) * g.pstride + (int64_t)y * g.nz + z;
+  if (!Q16) {
+    float* p = reinterpret_cast<float*>(A.out) + off;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) p[c * g.cstride] = s[c];
+  } else {
+    float nz[10];
+    if (DITHER) {
+      const uint32_t gi = (uint32_t)(((int64_t)(g.gx0 + x) * g.gny + y) * g.gnz + z);
+      const uint32_t h0 = mix32(gi + A.step_key);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const uint32_t h = mix32(h0 ^ ((uint32_t)(k + 1) * 0x9E3779B9u));
+        nz[2 * k] = noise16(h & 0xFFFFu);
+        nz[2 * k + 1] = noise16(h >> 16);
+      }
+    }
+    uint32_t code[10];
+    bool any_sat = false;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) {
+      float t = __fmaf_rn(s[c], A.Q.enc_scale[c], A.Q.enc_off[c]);
+      if (DITHER) t += nz[c];
+      code[c] = min(f2u16_floor(t), A.Q.levels[c]);
+      const float r = __fmaf_rn(s[c], A.Q.sat_a[c], A.Q.sat_b[c]);
+      if (stat && !(fabsf(r) <= 1.0f)) {
+        atomicAdd(&A.stats->sat[c], 1ull);
+        any_sat = true;
+      }
+    }
+    (void)any_sat;
+    uint32_t* p = reinterpret_cast<uint32_t*>(A.out) + off;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) p[k * g.cstride] = __byte_perm(code[2 * k], code[2 * k + 1], 0x5410);
+  }
+  if (stat) {
+    red[0] += s[0]; red[1] += s[1]; red[2] += s[2]; red[3] += s[3];
+    const float inv = rcp_nr(1.0f + s[0]);
+    const float u2 = (s[1] * s[1] + s[2] * s[2] + s[3] * s[3]) * inv * inv;
+    red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
+  }
+}
+
+__device__ __forceinline__ void flush_stats(const StepArgs& A, float red[5]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) red[k] += __shfl_xor_sync(0xffffffffu, red[k], o);
+  float m = red[4];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (t > m || t != t) ? t : m;
+  }
+  if (lane == 0) {
+    atomicAdd(&A.stats->mass_dev, (double)red[0]);
+    atomicAdd(&A.stats->mom[0], (double)red[1]);
+    atomicAdd(&A.stats->mom[1], (double)red[2]);
+    atomicAdd(&A.stats->mom[2], (double)red[3]);
+    atomicMax(&A.stats->max_u2_bits, __float_as_uint(m));
+  }
+}
+
+// mode 0: pull update of listed (or all) fluid cells; mode 1: reset listed solid cells to rest
+template <bool Q16, bool FORCE, bool DITHER>
+__global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepArgs A,
+                                                  const int64_t* __restrict__ cells,
+                                                  const uint32_t* __restrict__ masks, int64_t n,
+                                                  int mode) {
+  const Geo& g = A.g;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  if (idx < n) {
+    const int64_t cell = cells ? cells[idx] : idx;
+    const int64_t yz = (int64_t)g.ny * g.nz;
+    const int x = (int)(cell / yz);
+    const int64_t r = cell - (int64_t)x * yz;
+    const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
+    float s[10];
+    if (mode == 1) {
+#pragma unroll
+      for (int c = 0; c < 10; ++c) s[c] = 0.f;
+    } else {
+      const uint32_t mask = masks ? masks[idx] : 0u;
+      float m[10];
+#pragma unroll
+      for (int c = 0; c < 10; ++c) m[c] = 0.f;
+      PullAll<0, Q16, FORCE>::run(A, x, y, z, mask, m);
+      raw_to_state<float>(m, s);
+    }
+    store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && mode == 0, red);
+  }
+  if (A.do_stats && mode == 0) flush_stats(A, red);
+}
+
+cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
+                              int64_t n, int mode, bool q16, bool force, bool dither,
+                              cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int tpb = 128;
+  const int64_t nb = (n + tpb - 1) / tpb;
+#define HLBM_PULL(Q, F, D)                                                                      \
+  if (q16 == Q && force == F && dither == D) {                                                  \
+    pull_cells<Q, F, D><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, mode);               \
+    return cudaGetLastError();                                                                  \
+  }
+  HLBM_PULL(false, false, false)
+  HLBM_PULL(false, true, false)
+  HLBM_PULL(true, false, false)
+  HLBM_PULL(true, true, false)
+  HLBM_PULL(true, false, true)
+  HLBM_PULL(true, true, true)
+#undef HLBM_PULL
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ mask -> lists
+// solid flag on the padded grid; mask_ext holds local planes -1..nx (x-ghosts already resolved
+// by the host per the x BCs / neighbouring slabs); y/z: wall ghost = solid, else periodic wrap.
+// Order of the checks mirrors oracle/step.py:padded_solid (x padded first, then y, then z).
+__device__ __forceinline__ bool padded_solid(const uint8_t* mask_ext, const MaskGeo& m, int x, int y,
+                                             int z) {
+  if (z < 0) { if (m.bc_zwall_lo) return true; z += m.nz; }
+  else if (z >= m.nz) { if (m.bc_zwall_hi) return true; z -= m.nz; }
+  if (y < 0) { if (m.bc_ywall_lo) return true; y += m.ny; }
+  else if (y >= m.ny) { if (m.bc_ywall_hi) return true; y -= m.ny; }
+  return mask_ext[((int64_t)(x + 1) * m.ny + y) * m.nz + z] != 0;
+}
+
+// per cell: link mask (fluid cells) and class flags: bit0 boundary, bit1 solid
+__global__ void classify_cells(const uint8_t* __restrict__ mask_ext, MaskGeo m,
+                               uint32_t* __restrict__ links, uint8_t* __restrict__ cls) {
+  const int64_t n = (int64_t)m.nx * m.ny * m.nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i / ((int64_t)m.ny * m.nz));
+    const int64_t r = i - (int64_t)x * m.ny * m.nz;
+    const int y = (int)(r / m.nz), z = (int)(r - (int64_t)y * m.nz);
+    const bool solid = mask_ext[i + (int64_t)m.ny * m.nz] != 0;
+    uint32_t lm = 0;
+    if (!solid) {
+#pragma unroll
+      for (int k = 1; k < 27; ++k)
+        if (padded_solid(mask_ext, m, x - kCX[k], y - kCY[k], z - kCZ[k])) lm |= 1u << k;
+    }
+    links[i] = lm;
+    cls[i] = (uint8_t)((lm != 0 ? 1 : 0) | (solid ? 2 : 0));
+  }
+}
+
+constexpr int kCompactTPB = 256;
+constexpr int kCompactPer = 16;   // cells per thread per tile
+constexpr int kCompactTile = kCompactTPB * kCompactPer;
+
+// counts[b] = number of cells in tile b with (cls & want)
+__global__ void compact_count(const uint8_t* __restrict__ cls, int64_t n, uint8_t want,
+                              int64_t* __restrict__ counts) {
+  __shared__ int warp_tot[kCompactTPB / 32];
+  const int64_t base = (int64_t)blockIdx.x * kCompactTile;
+  int c = 0;
+  for (int k = 0; k < kCompactPer; ++k) {
+    const int64_t i = base + (int64_t)k * kCompactTPB + threadIdx.x;
+    if (i < n && (cls[i] & want)) ++c;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < kCompactTPB / 32; ++w) t += warp_tot[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of the per-tile counts (single CTA, sequential chunks)
+__global__ void compact_scan(int64_t* __restrict__ counts, int64_t nblocks, int64_t* __restrict__ total) {
+  __shared__ int64_t carry;
+  __shared__ int64_t buf[1024];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nblocks; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < nblocks ? counts[i] : 0;
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const int64_t t = threadIdx.x >= o ? buf[threadIdx.x - o] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < nblocks) counts[i] = carry + buf[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += buf[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// ordered scatter: within a tile, cells keep increasing linear index order
+__global__ void compact_scatter(const uint8_t* __restrict__ cls, const uint32_t* __restrict__ links,
+                                int64_t n, uint8_t want, const int64_t* __restrict__ offsets,
+                                int64_t* __restrict__ out_cells, uint32_t* __restrict__ out_masks) {
+  __shared__ int warp_tot[kCompactTPB / 32];
+  __shared__ int64_t running;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kCompactTile;
+  if (threadIdx.x == 0) running = offsets[blockIdx.x];
+  __syncthreads();
+  for (int k = 0; k < kCompactPer; ++k) {
+    const int64_t i = base + (int64_t)k * kCompactTPB + threadIdx.x;
+    const bool f = i < n && (cls[i] & want);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) warp_tot[w] = __popc(bal);
+    __syncthreads();
+    int64_t pre = running;
+    for (int j = 0; j < w; ++j) pre += warp_tot[j];
+    if (f) {
+      const int64_t pos = pre + __popc(bal & ((1u << lane) - 1u));
+      out_cells[pos] = i;
+      if (out_masks) out_masks[pos] = links[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int j = 0; j < kCompactTPB / 32; ++j) t += warp_tot[j];
+      running += t;
+    }
+    __syncthreads();
+  }
+}
+
+// bitmask of special (boundary or solid) cells, one u32 word per 32 z-cells of a row
+__global__ void special_bits_kernel(const uint8_t* __restrict__ cls, int nx, int ny, int nz, int row_words,
+                                    uint32_t* __restrict__ bits) {
+  const int64_t nwords = (int64_t)nx * ny * row_words;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / row_words;
+    const int wz = (int)(i - row * row_words);
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int z = wz * 32 + b;
+      if (z < nz && cls[row * nz + z]) v |= 1u << b;
+    }
+    bits[i] = v;
+  }
+}
+
+// ------------------------------------------------------------------ import / export
+// Exact float64 ranges for the codec (the SPEC quantizer is evaluated in float64 on import /
+// export so that set_moments -> get_moments reproduces oracle/codec.py bit-for-bit).
+
+// planes [x0, x0+cnt) of the interior; inputs are device copies of the reference layout
+// (rho[cnt][ny][nz], mom[3][cnt][ny][nz], stress[6][cnt][ny][nz], float64)
+template <bool Q16>
+__global__ void import_f64(Geo g, Ranges R, void* dst, const double* __restrict__ rho,
+                           const double* __restrict__ mom, const double* __restrict__ stress, int x0,
+                           int cnt, unsigned long long* __restrict__ sat) {
+  const int64_t yz = (int64_t)g.ny * g.nz, n = yz * cnt;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int xl = (int)(i / yz);
+    const int64_t r = i - (int64_t)xl * yz;
+    const double rh = rho[i];
+    const double j0 = mom[i], j1 = mom[n + i], j2 = mom[2 * n + i];
+    // sneq = stress - mom mom / rho  (moments.py:93-96, _outer_voigt :124-133)
+    const double v[10] = {rh,
+                          j0,
+                          j1,
+                          j2,
+                          stress[i] - j0 * j0 / rh,
+                          stress[n + i] - j0 * j1 / rh,
+                          stress[2 * n + i] - j0 * j2 / rh,
+                          stress[3 * n + i] - j1 * j1 / rh,
+                          stress[4 * n + i] - j1 * j2 / rh,
+                          stress[5 * n + i] - j2 * j2 / rh};
+    const int64_t off = (int64_t)(x0 + xl + 1) * g.pstride + r;
+    if (!Q16) {
+      float* p = reinterpret_cast<float*>(dst) + off;
+      p[0] = (float)(rh - 1.0);
+      for (int c = 1; c < 10; ++c) p[c * g.cstride] = (float)v[c];
+    } else {
+      uint32_t code[10];
+      for (int c = 0; c < 10; ++c) {
+        // m' = (clamp(m) - min)/(max - min); q = floor(m'(2^b-1) + 1/2)
+        const double m = v[c];
+        if (sat && (m < R.mn[c] || m > R.mx[c])) atomicAdd(&sat[c], 1ull);
+        const double mc = fmin(fmax(m, R.mn[c]), R.mx[c]);
+        const double t = (mc - R.mn[c]) / (R.mx[c] - R.mn[c]) * R.levels[c] + 0.5;
+        code[c] = (uint32_t)fmin(fmax(floor(t), 0.0), R.levels[c]);
+      }
+      uint32_t* p = reinterpret_cast<uint32_t*>(dst) + off;
+      for (int k = 0; k < 5; ++k) p[k * g.cstride] = code[2 * k] | (code[2 * k + 1] << 16);
+    }
+  }
+}
+
+// export a box [x0,x0+cx) x [y0,y0+cy) x [z0,z0+cz) of the interior (y, z wrap periodically)
+template <bool Q16>
+__global__ void export_f64(Geo g, Ranges R, const void* src, double* __restrict__ rho,
+                           double* __restrict__ mom, double* __restrict__ stress, int x0, int cx, int y0,
+                           int cy, int z0, int cz) {
+  const int64_t n = (int64_t)cx * cy * cz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int xl = (int)(i / ((int64_t)cy * cz));
+    const int64_t r = i - (int64_t)xl * cy * cz;
+    const int yl = (int)(r / cz), zl = (int)(r - (int64_t)yl * cz);
+    const int y = wrapi(y0 + yl, g.ny), z = wrapi(z0 + zl, g.nz);
+    const int64_t off = (int64_t)(x0 + xl + 1) * g.pstride + (int64_t)y * g.nz + z;
+    double v[10];
+    if (!Q16) {
+      const float* p = reinterpret_cast<const float*>(src) + off;
+      for (int c = 0; c < 10; ++c) v[c] = (double)p[c * g.cstride];
+      v[0] += 1.0;
+    } else {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(src) + off;
+      for (int k = 0; k < 5; ++k) {
+        const uint32_t wv = p[k * g.cstride];
+        // m = min + q (max - min)/(2^b - 1)
+        v[2 * k] = R.mn[2 * k] + (double)(wv & 0xFFFFu) * ((R.mx[2 * k] - R.mn[2 * k]) / R.levels[2 * k]);
+        v[2 * k + 1] =
+            R.mn[2 * k + 1] + (double)(wv >> 16) * ((R.mx[2 * k + 1] - R.mn[2 * k + 1]) / R.levels[2 * k + 1]);
+      }
+    }
+    const double rh = v[0], j0 = v[1], j1 = v[2], j2 = v[3];
+    rho[i] = rh;
+    mom[i] = j0;
+    mom[n + i] = j1;
+    mom[2 * n + i] = j2;
+    // stress = sneq + mom mom / rho   (neq_recompose, moments.py:99-102)
+    stress[i] = v[4] + j0 * j0 / rh;
+    stress[n + i] = v[5] + j0 * j1 / rh;
+    stress[2 * n + i] = v[6] + j0 * j2 / rh;
+    stress[3 * n + i] = v[7] + j1 * j1 / rh;
+    stress[4 * n + i] = v[8] + j1 * j2 / rh;
+    stress[5 * n + i] = v[9] + j2 * j2 / rh;
+  }
+}
+
+// rho = rho0, u = sum_m a_m sin(2 pi k_m . x_global / N + phi_m), sneq = 0; modes are
+// 7 doubles (kx, ky, kz, ax, ay, az, phi).  Used for the synthetic turbulence box.
+template <bool Q16>
+__global__ void init_modes(Geo g, Ranges R, void* dst, double rho0, const double* __restrict__ modes,
+                           int nmodes) {
+  const int64_t yz = (int64_t)g.ny * g.nz, n = yz * g.nx;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i / yz);
+    const int64_t r = i - (int64_t)x * yz;
+    const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
+    const int gx = g.gx0 + x;
+    double u[3] = {0.0, 0.0, 0.0};
+    for (int m = 0; m < nmodes; ++m) {
+      const double* md = modes + 7 * m;
+      // phase in turns, reduced exactly before the float sincos
+      double t = md[0] * gx / (double)g.gnx_total + md[1] * y / (double)g.gny + md[2] * z / (double)g.gnz;
+      t -= floor(t);
+      const float sn = sinpif((float)(2.0 * t + md[6] / 3.141592653589793));
+      u[0] += md[3] * sn;
+      u[1] += md[4] * sn;
+      u[2] += md[5] * sn;
+    }
+    const double v[10] = {rho0, rho0 * u[0], rho0 * u[1], rho0 * u[2], 0, 0, 0, 0, 0, 0};
+    const int64_t off = (int64_t)(x + 1) * g.pstride + r;
+    if (!Q16) {
+      float* p = reinterpret_cast<float*>(dst) + off;
+      p[0] = (float)(rho0 - 1.0);
+      for (int c = 1; c < 10; ++c) p[c * g.cstride] = (float)v[c];
+    } else {
+      uint32_t code[10];
+      for (int c = 0; c < 10; ++c) {
+        const double mc = fmin(fmax(v[c], R.mn[c]), R.mx[c]);
+        const double t = (mc - R.mn[c]) / (R.mx[c] - R.mn[c]) * R.levels[c] + 0.5;
+        code[c] = (uint32_t)fmin(fmax(floor(t), 0.0), R.levels[c]);
+      }
+      uint32_t* p = reinterpret_cast<uint32_t*>(dst) + off;
+      for (int k = 0; k < 5; ++k) p[k * g.cstride] = code[2 * k] | (code[2 * k + 1] << 16);
+    }
+  }
+}
+
+template __global__ void import_f64<false>(Geo, Ranges, void*, const double*, const double*, const double*, int, int, unsigned long long*);
+template __global__ void import_f64<true>(Geo, Ranges, void*, const double*, const double*, const double*, int, int, unsigned long long*);
+
+}  // namespace hlbm
+
+// ------------------------------------------------------------------ host-side launchers
+namespace hlbm {
+
+static unsigned grid_for(int64_t n, int tpb) {
+  int64_t b = (n + tpb - 1) / tpb;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
+                          const double* mom, const double* stress, int x0, int cnt,
+                          unsigned long long* sat, cudaStream_t st) {
+  const int64_t n = (int64_t)g.ny * g.nz * cnt;
+  if (q16) import_f64<true><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho, mom, stress, x0, cnt, sat);
+  else import_f64<false><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho, mom, stress, x0, cnt, sat);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export(const Geo& g, const Ranges& R, bool q16, const void* src, double* rho,
+                          double* mom, double* stress, int x0, int cx, int y0, int cy, int z0, int cz,
+                          cudaStream_t st) {
+  const int64_t n = (int64_t)cx * cy * cz;
+  if (q16) export_f64<true><<<grid_for(n, 256), 256, 0, st>>>(g, R, src, rho, mom, stress, x0, cx, y0, cy, z0, cz);
+  else export_f64<false><<<grid_for(n, 256), 256, 0, st>>>(g, R, src, rho, mom, stress, x0, cx, y0, cy, z0, cz);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_modes(const Geo& g, bool q16, const Ranges& R, void* dst, double rho0,
+                              const double* modes, int nmodes, cudaStream_t st) {
+  const int64_t n = (int64_t)g.nx * g.ny * g.nz;
+  if (q16) init_modes<true><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho0, modes, nmodes);
+  else init_modes<false><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho0, modes, nmodes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_classify(const uint8_t* mask_ext, const MaskGeo& m, uint32_t* links, uint8_t* cls,
+                            cudaStream_t st) {
+  const int64_t n = (int64_t)m.nx * m.ny * m.nz;
+  classify_cells<<<grid_for(n, 256), 256, 0, st>>>(mask_ext, m, links, cls);
+  return cudaGetLastError();
+}
+
+int64_t compact_tiles(int64_t n) { return (n + kCompactTile - 1) / kCompactTile; }
+
+// counts must hold compact_tiles(n) entries, total one entry (device)
+cudaError_t launch_compact(const uint8_t* cls, const uint32_t* links, int64_t n, uint8_t want,
+                           int64_t* counts, int64_t* total, int64_t* out_cells, uint32_t* out_masks,
+                           bool count_only, cudaStream_t st) {
+  const int64_t nt = compact_tiles(n);
+  if (nt == 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), st);
+  if (count_only) {
+    compact_count<<<(unsigned)nt, kCompactTPB, 0, st>>>(cls, n, want, counts);
+    compact_scan<<<1, 1024, 0, st>>>(counts, nt, total);
+  } else {
+    compact_scatter<<<(unsigned)nt, kCompactTPB, 0, st>>>(cls, links, n, want, counts, out_cells, out_masks);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_special_bits(const uint8_t* cls, int nx, int ny, int nz, int row_words,
+                                uint32_t* bits, cudaStream_t st) {
+  const int64_t n = (int64_t)nx * ny * row_words;
+  special_bits_kernel<<<grid_for(n, 256), 256, 0, st>>>(cls, nx, ny, nz, row_words, bits);
+  return cudaGetLastError();
+}
+
+}  // namespace hlbm

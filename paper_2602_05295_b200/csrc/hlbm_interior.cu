@@ -1,0 +1,493 @@
+// fluid_interior: the split scheme's divergence-free fluid update (Alg. 2, lines
+// 340-357) over every cell of a slab, sm_100a.
+//
+// Per cell:  load stored moments -> moment-space collision (collision.py:137-194) ->
+// third-order Hermite reconstruction of the 27 post-collision populations (moments.py:64-90)
+// -> pull streaming f_i(x) <- f_i(x - c_i) -> moment extraction
+// (moments.py:25-39) -> neq split (moments.py:93-96) -> store (fp32 or 16-bit codes).
+//
+// Mapping:
+//   * CTA = 16 warps; warp w holds y row (y0 - 1 + w); rows 1..14 are written, rows 0/15 are
+//     halo rows that only produce the populations their neighbour needs.
+//   * lane l holds the z pair (zb + 2l, zb + 2l + 1); every arithmetic op is packed f32x2
+//     (FFMA2/FADD2/FMUL2).  Cells zb+1 .. zb+60 are written.
+//   * the CTA marches along x over a segment; the x-direction of streaming is a register
+//     rotation (two 10-moment accumulators), never a memory exchange.
+//   * streaming is sum-factorised by axis: z shifts are warp shuffles, y shifts exchange 18
+//     f32x2 per lane through shared memory, x shifts are the marching accumulators.
+//   * input planes are staged into shared memory by 1-D bulk TMA copies (cp.async.bulk +
+//     mbarrier), STAGES planes ahead of the consumer.
+#include "hlbm_params.cuh"
+
+namespace hlbm {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HLBM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HLBM_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int slot_of(int cx, int cy, int kz) {
+  return ((cx + 1) * 2 + (cy > 0 ? 0 : 1)) * 3 + kz;
+}
+
+// value of P at the shifted pair: lane's cells take the neighbour at z-1 / z+1
+__device__ __forceinline__ V from_zm(V v) {   // value at (z - 1) for both cells
+  float up = __shfl_up_sync(0xffffffffu, v.y, 1);
+  return make_float2(up, v.x);
+}
+__device__ __forceinline__ V from_zp(V v) {   // value at (z + 1)
+  float dn = __shfl_down_sync(0xffffffffu, v.x, 1);
+  return make_float2(v.y, dn);
+}
+
+template <int NC, int STAGES>
+struct Smem {
+  uint32_t stage[STAGES][NC][kNW][kZW];
+  V exch[kNSlot][kNW][32];
+  uint64_t bar[STAGES];
+  float red[kNW][5];
+};
+
+// Producer: warp 0 issues the bulk copies of source plane p into one stage.
+template <int NC>
+__device__ __forceinline__ void issue_plane(const StepArgs& A, int p, uint32_t (*stage)[kNW][kZW],
+                                            uint64_t* bar, int zb, int y0, int lane) {
+  const Geo& g = A.g;
+  int sp;
+  if (p < 0) sp = g.x_lo_src;
+  else if (p >= g.nx) sp = g.x_hi_src;
+  else sp = p + 1;
+  const bool inflow = sp < 0;
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(bar, inflow ? 0u : (uint32_t)(NC * kNW * kZW * 4));
+  }
+  __syncwarp();
+  if (inflow) return;
+  const uint32_t* base = reinterpret_cast<const uint32_t*>(A.in) + (int64_t)sp * g.pstride;
+  for (int r = lane; r < NC * kNW; r += 32) {
+    const int c = r / kNW, w = r - c * kNW;
+    const int y = wrapi(y0 - 1 + w, g.ny);
+    const uint32_t* row = base + c * g.cstride + (int64_t)y * g.nz;
+    uint32_t* dst = stage[c][w];
+    int z = zb, done = 0;
+    while (done < kZW) {
+      const int n = min(kZW - done, g.nz - z);
+      bulk_g2s(dst + done, row + z, (uint32_t)n * 4u, bar);
+      done += n;
+      z = 0;
+    }
+  }
+}
+
+// Partial moments of one destination plane.  Index order of the 6 "kx=0" moments:
+// (ky,kz) = 00, 01, 02, 10, 11, 20.  A plane that has received the cx=+1 contribution
+// of source q-1 and the cx=0 contribution of source q carries 9 values (a: kx=0,
+// b: kx=1 for (ky,kz) = 00, 01, 10; the kx=2 partial equals b[0]).
+struct Part9 {
+  V a[6];
+  V b[3];
+};
+struct Part6 {   // only the cx=+1 contribution of source q-1: kx=1/kx=2 partials are copies
+  V a[6];
+};
+
+// ---------------------------------------------------------------------------------------
+// reconstruction of the 9 populations with a given cx, z-stage, hand-off of the cy = +-1
+// results to shared memory; returns the cy = 0 results g[kz] (added to the x accumulators
+// before the barrier so nothing but the accumulators is live across it).
+template <int CX>
+__device__ __forceinline__ void recon_cx(const Coef<V>& C, bool need_p, bool need_0, bool need_m,
+                                         V (*exch)[kNW][32], int w, int lane, V g0out[3]) {
+  V G00, G10, G20, G01, G11, G21, G02, G12;
+  if (CX == 0) {
+    const float f4 = 4.0f;
+    G00 = vmul(C.K0, f4); G10 = vmul(C.Ly, f4); G20 = vmul(C.Qyy, f4);
+    G01 = vmul(C.Lz, f4); G11 = vmul(C.Qyz, f4); G21 = vmul(C.Tyyz, f4);
+    G02 = vmul(C.Qzz, f4); G12 = vmul(C.Tyzz, f4);
+  } else if (CX > 0) {
+    G00 = vadd(vadd(C.K0, C.Qxx), C.Lx); G10 = vadd(vadd(C.Ly, C.Txxy), C.Qxy);
+    G20 = vadd(C.Qyy, C.Txyy);
+    G01 = vadd(vadd(C.Lz, C.Txxz), C.Qxz); G11 = vadd(C.Qyz, C.Txyz); G21 = C.Tyyz;
+    G02 = vadd(C.Qzz, C.Txzz); G12 = C.Tyzz;
+  } else {
+    G00 = vsub(vadd(C.K0, C.Qxx), C.Lx); G10 = vsub(vadd(C.Ly, C.Txxy), C.Qxy);
+    G20 = vsub(C.Qyy, C.Txyy);
+    G01 = vsub(vadd(C.Lz, C.Txxz), C.Qxz); G11 = vsub(C.Qyz, C.Txyz); G21 = C.Tyyz;
+    G02 = vsub(C.Qzz, C.Txzz); G12 = C.Tyzz;
+  }
+#pragma unroll
+  for (int cyi = 0; cyi < 3; ++cyi) {
+    const int CY = (cyi == 0) ? 1 : (cyi == 1 ? -1 : 0);   // +1, -1, then 0
+    if (CY > 0 && !need_p) continue;
+    if (CY < 0 && !need_m) continue;
+    if (CY == 0 && !need_0) continue;
+    V B0, B1, B2;
+    if (CY == 0) {
+      B0 = vmul(G00, 4.0f); B1 = vmul(G01, 4.0f); B2 = vmul(G02, 4.0f);
+    } else if (CY > 0) {
+      B0 = vadd(vadd(G00, G20), G10); B1 = vadd(vadd(G01, G21), G11); B2 = vadd(G02, G12);
+    } else {
+      B0 = vsub(vadd(G00, G20), G10); B1 = vsub(vadd(G01, G21), G11); B2 = vsub(G02, G12);
+    }
+    // cz level: ft(cz=0) = 4 B0, ft(+-1) = (B0 + B2) +- B1
+    const V f0 = vmul(B0, 4.0f);
+    const V t = vadd(B0, B2);
+    const V fp = vadd(t, B1), fm = vsub(t, B1);
+    // z-stage (pull): cz=+1 comes from z-1, cz=-1 from z+1
+    const V P = from_zm(fp), M = from_zp(fm);
+    const V T2 = vadd(P, M);
+    const V g0 = vadd(f0, T2), g1 = vsub(P, M), g2 = T2;
+    if (CY == 0) {
+      g0out[0] = g0; g0out[1] = g1; g0out[2] = g2;
+    } else {
+      exch[slot_of(CX, CY, 0)][w][lane] = g0;
+      exch[slot_of(CX, CY, 1)][w][lane] = g1;
+      exch[slot_of(CX, CY, 2)][w][lane] = g2;
+    }
+  }
+}
+
+// y-stage for one cx: neighbour contributions (row y-1 sent cy=+1, row y+1 sent cy=-1)
+// as t = A + B (even in cy) and d = A - B (odd in cy), per kz.
+template <int CX>
+__device__ __forceinline__ void ystage(V (*exch)[kNW][32], int w, int lane, V t[3], V d[2]) {
+  const V A0 = exch[slot_of(CX, 1, 0)][w - 1][lane];
+  const V A1 = exch[slot_of(CX, 1, 1)][w - 1][lane];
+  const V A2 = exch[slot_of(CX, 1, 2)][w - 1][lane];
+  const V B0 = exch[slot_of(CX, -1, 0)][w + 1][lane];
+  const V B1 = exch[slot_of(CX, -1, 1)][w + 1][lane];
+  const V B2 = exch[slot_of(CX, -1, 2)][w + 1][lane];
+  t[0] = vadd(A0, B0); t[1] = vadd(A1, B1); t[2] = vadd(A2, B2);
+  d[0] = vsub(A0, B0); d[1] = vsub(A1, B1);
+}
+
+// ---------------------------------------------------------------------------------------
+template <bool Q16>
+__device__ __forceinline__ void load_state(const uint32_t (*st)[kNW][kZW], int w, int lane,
+                                           bool inflow, const StepArgs& A, V s[10]) {
+  if (inflow) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s[c] = vsplat(A.inflow[c]);
+    return;
+  }
+  if (!Q16) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s[c] = *reinterpret_cast<const V*>(&st[c][w][2 * lane]);
+  } else {
+    const V two23 = vsplat(8388608.0f);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint2 wv = *reinterpret_cast<const uint2*>(&st[k][w][2 * lane]);
+      const V lo = make_float2(code_lo_f(wv.x), code_lo_f(wv.y));
+      const V hi = make_float2(code_hi_f(wv.x), code_hi_f(wv.y));
+      s[2 * k] = vfma(vsub(lo, two23), vsplat(A.Q.dec_step[2 * k]), vsplat(A.Q.dec_off[2 * k]));
+      s[2 * k + 1] =
+          vfma(vsub(hi, two23), vsplat(A.Q.dec_step[2 * k + 1]), vsplat(A.Q.dec_off[2 * k + 1]));
+    }
+  }
+}
+
+// store of one finished cell pair + fused statistics
+template <bool Q16, bool DITHER>
+__device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z0,
+                                           bool wx, bool wy, bool statx, bool staty, float red[5]) {
+  const Geo& g = A.g;
+  V s[10];
+  raw_to_state(m, s);
+  const int64_t off = (int64_t)(q + 1) * g.pstride + (int64_t)y * g.nz + z0;
+  if (!Q16) {
+    float* out = reinterpret_cast<float*>(A.out) + off;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) {
+      float* p = out + c * g.cstride;
+      if (wx && wy) *reinterpret_cast<V*>(p) = s[c];
+      else if (wx) p[0] = s[c].x;
+      else if (wy) p[1] = s[c].y;
+    }
+  } else {
+    uint32_t code[10][2];
+    float mx0 = 0.f, mx1 = 0.f;
+    V nz[10];
+    if (DITHER) {
+      const uint32_t gi = (uint32_t)(((int64_t)(g.gx0 + q) * g.gny + y) * g.gnz + z0);
+      const uint32_t h0a = mix32(gi + A.step_key), h0b = mix32(gi + 1u + A.step_key);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const uint32_t kk = (uint32_t)(k + 1) * 0x9E3779B9u;
+        const uint32_t ha = mix32(h0a ^ kk), hb = mix32(h0b ^ kk);
+        nz[2 * k] = make_float2(noise16(ha & 0xFFFFu), noise16(hb & 0xFFFFu));
+        nz[2 * k + 1] = make_float2(noise16(ha >> 16), noise16(hb >> 16));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 10; ++c) {
+      V t = vfma(s[c], vsplat(A.Q.enc_scale[c]), vsplat(A.Q.enc_off[c]));
+      if (DITHER) t = vadd(t, nz[c]);
+      const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+      mx0 = fmaxf(mx0, fabsf(r.x));
+      mx1 = fmaxf(mx1, fabsf(r.y));
+      code[c][0] = min(f2u16_floor(t.x), A.Q.levels[c]);
+      code[c][1] = min(f2u16_floor(t.y), A.Q.levels[c]);
+    }
+    uint32_t* out = reinterpret_cast<uint32_t*>(A.out) + off;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      uint32_t* p = out + k * g.cstride;
+      const uint32_t w0 = __byte_perm(code[2 * k][0], code[2 * k + 1][0], 0x5410);
+      const uint32_t w1 = __byte_perm(code[2 * k][1], code[2 * k + 1][1], 0x5410);
+      if (wx && wy) *reinterpret_cast<uint2*>(p) = make_uint2(w0, w1);
+      else if (wx) p[0] = w0;
+      else if (wy) p[1] = w1;
+    }
+    // saturation: |r| > 1  <=>  m outside [min, max]  (rare slow path)
+    const bool satx = statx && !(mx0 <= 1.0f), saty = staty && !(mx1 <= 1.0f);
+    if (satx || saty) {
+#pragma unroll
+      for (int c = 0; c < 10; ++c) {
+        const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+        const unsigned n = (satx && !(fabsf(r.x) <= 1.0f)) + (saty && !(fabsf(r.y) <= 1.0f));
+        if (n) atomicAdd(&A.stats->sat[c], (unsigned long long)n);
+      }
+    }
+  }
+  if (statx) {
+    red[0] += s[0].x; red[1] += s[1].x; red[2] += s[2].x; red[3] += s[3].x;
+    const float inv = rcp_nr(1.0f + s[0].x);
+    const float u2 = (s[1].x * s[1].x + s[2].x * s[2].x + s[3].x * s[3].x) * inv * inv;
+    red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
+  }
+  if (staty) {
+    red[0] += s[0].y; red[1] += s[1].y; red[2] += s[2].y; red[3] += s[3].y;
+    const float inv = rcp_nr(1.0f + s[0].y);
+    const float u2 = (s[1].y * s[1].y + s[2].y * s[2].y + s[3].y * s[3].y) * inv * inv;
+    red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
+  }
+}
+
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, int STAGES>
+__global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_constant__ StepArgs A) {
+  constexpr int NC = Q16 ? 5 : 10;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem<NC, STAGES>& S = *reinterpret_cast<Smem<NC, STAGES>*>(smem_raw);
+  const Geo& g = A.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+  int item = blockIdx.x;
+  const int zt = item % g.nzt;
+  item /= g.nzt;
+  const int yt = item % g.nyt;
+  const int xsi = item / g.nyt;
+  const int zb = zt * kZT;
+  const int zlo = zb + 1, zhi = min(zb + 1 + kZT, g.nz + 1);
+  const int y0 = yt * kRows;
+  const int yrow_u = y0 - 1 + w;
+  const int yrow = wrapi(yrow_u, g.ny);
+  const bool row_interior = (w >= 1) && (w <= kRows) && (yrow_u < g.ny);
+  const int xs = xsi * g.xseg, xe = min(xs + g.xseg, g.nx);
+  const int NP = xe - xs + 2;
+  const bool need_p = (w < kNW - 1);   // this row feeds row+1 (cy = +1)
+  const bool need_m = (w > 0);         // feeds row-1 (cy = -1)
+  const bool need_0 = (w > 0) && (w < kNW - 1);
+
+  // this lane's cells
+  const int zu0 = zb + 2 * lane;
+  const int z0 = wrapi(zu0, g.nz);
+  const bool wx = row_interior && zu0 >= zlo && zu0 < zhi;
+  const bool wy = row_interior && zu0 + 1 >= zlo && zu0 + 1 < zhi;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (w == 0) {
+    for (int it = 0; it < STAGES - 1 && it < NP; ++it)
+      issue_plane<NC>(A, xs - 1 + it, S.stage[it % STAGES], &S.bar[it % STAGES], zb, y0, lane);
+  }
+
+  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  Part9 Ac;   // dest p-1 partial
+  Part6 Bc;   // dest p partial
+#pragma unroll
+  for (int k = 0; k < 6; ++k) Ac.a[k] = Bc.a[k] = vsplat(0.f);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
+
+  auto body = [&](int it, Part9& A9, Part6& B6) {
+    const int p = xs - 1 + it;
+    if (w == 0 && it + STAGES - 1 < NP) {
+      const int j = it + STAGES - 1;
+      issue_plane<NC>(A, xs - 1 + j, S.stage[j % STAGES], &S.bar[j % STAGES], zb, y0, lane);
+    }
+    const int q = p - 1;   // destination plane finished in this iteration
+    const bool store_plane = row_interior && q >= xs && q < xe;
+    uint32_t sbits = 0;
+    if (SPECIAL && store_plane) {
+      const int64_t bi = ((int64_t)q * g.ny + yrow) * A.bits_row_words + (z0 >> 5);
+      sbits = __ldg(A.special_bits + bi) >> (z0 & 31);
+    }
+    const int sp = (p < 0) ? g.x_lo_src : (p >= g.nx ? g.x_hi_src : p + 1);
+    const bool inflow = sp < 0;
+    mbar_wait(&S.bar[it % STAGES], (uint32_t)((it / STAGES) & 1));
+    V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
+    Part9 nb;    // dest p after this source
+    V nn[6];     // dest p+1 after this source
+    {
+      V s[10];
+      load_state<Q16>(S.stage[it % STAGES], w, lane, inflow, A, s);
+      const Coef<V> C =
+          coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+      V gz[3];
+      // cx = -1 -> dest q (final contribution)
+      gz[0] = gz[1] = gz[2] = vsplat(0.f);
+      recon_cx<-1>(C, need_p, need_0, need_m, S.exch, w, lane, gz);
+      fin[0] = vadd(A9.a[0], gz[0]);
+      fin[3] = vadd(A9.a[1], gz[1]);
+      fin[9] = vadd(A9.a[2], gz[2]);
+      fin[2] = A9.a[3];
+      fin[8] = A9.a[4];
+      fin[7] = A9.a[5];
+      fin[1] = vsub(A9.b[0], gz[0]);
+      fin[6] = vsub(A9.b[1], gz[1]);
+      fin[5] = A9.b[2];
+      fin[4] = vadd(A9.b[0], gz[0]);
+      // cx = 0 -> dest p
+      recon_cx<0>(C, need_p, need_0, need_m, S.exch, w, lane, gz);
+      nb.a[0] = vadd(B6.a[0], gz[0]);
+      nb.a[1] = vadd(B6.a[1], gz[1]);
+      nb.a[2] = vadd(B6.a[2], gz[2]);
+      nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
+      nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
+      // cx = +1 -> dest p+1
+      recon_cx<1>(C, need_p, need_0, need_m, S.exch, w, lane, gz);
+      nn[0] = gz[0]; nn[1] = gz[1]; nn[2] = gz[2];
+    }
+    __syncthreads();
+    if (row_interior) {
+      V t[3], d[2];
+      ystage<-1>(S.exch, w, lane, t, d);
+      fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
+      fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
+      fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
+      fin[4] = vadd(fin[4], t[0]);
+      ystage<0>(S.exch, w, lane, t, d);
+      nb.a[0] = vadd(nb.a[0], t[0]); nb.a[1] = vadd(nb.a[1], t[1]); nb.a[2] = vadd(nb.a[2], t[2]);
+      nb.a[3] = vadd(nb.a[3], d[0]); nb.a[4] = vadd(nb.a[4], d[1]); nb.a[5] = vadd(nb.a[5], t[0]);
+      ystage<1>(S.exch, w, lane, t, d);
+      nn[0] = vadd(nn[0], t[0]); nn[1] = vadd(nn[1], t[1]); nn[2] = vadd(nn[2], t[2]);
+      nn[3] = d[0]; nn[4] = d[1]; nn[5] = t[0];
+      if (store_plane) {
+        const bool sx = A.do_stats && wx && !(SPECIAL && (sbits & 1u));
+        const bool sy = A.do_stats && wy && !(SPECIAL && (sbits & 2u));
+        store_pair<Q16, DITHER>(A, fin, q, yrow, z0, wx, wy, sx, sy, red);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { A9.a[k] = nb.a[k]; B6.a[k] = nn[k]; }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) A9.b[k] = nb.b[k];
+    __syncthreads();
+  };
+
+  for (int it = 0; it < NP; ++it) body(it, Ac, Bc);
+
+  if (A.do_stats) {
+    // block reduction of the fused statistics
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float v = red[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      red[k] = v;
+    }
+    float m = red[4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float t = __shfl_xor_sync(0xffffffffu, m, o);
+      m = (t > m || t != t) ? t : m;
+    }
+    red[4] = m;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) S.red[w][k] = red[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a[4] = {0, 0, 0, 0};
+      float mm = 0.f;
+      for (int i = 0; i < kNW; ++i) {
+        for (int k = 0; k < 4; ++k) a[k] += (double)S.red[i][k];
+        const float t = S.red[i][4];
+        mm = (t > mm || t != t) ? t : mm;
+      }
+      atomicAdd(&A.stats->mass_dev, a[0]);
+      atomicAdd(&A.stats->mom[0], a[1]);
+      atomicAdd(&A.stats->mom[1], a[2]);
+      atomicAdd(&A.stats->mom[2], a[3]);
+      atomicMax(&A.stats->max_u2_bits, __float_as_uint(mm));
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ host launcher
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER>
+static cudaError_t launch_t(const StepArgs& A, int nblocks, cudaStream_t st) {
+  constexpr int STAGES = Q16 ? 4 : 3;
+  constexpr int NC = Q16 ? 5 : 10;
+  const size_t smem = sizeof(Smem<NC, STAGES>);
+  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<nblocks, kNW * 32, smem, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
+                                  cudaStream_t st) {
+  const int nblocks = A.g.nzt * A.g.nyt * A.g.nxs;
+  if (nblocks == 0) return cudaSuccess;
+#define HLBM_DISPATCH(Q, F, S, D)                                              \
+  if (q16 == Q && force == F && special == S && dither == D)                   \
+    return launch_t<Q, F, S, D>(A, nblocks, st);
+  HLBM_DISPATCH(false, false, false, false)
+  HLBM_DISPATCH(false, false, true, false)
+  HLBM_DISPATCH(false, true, false, false)
+  HLBM_DISPATCH(false, true, true, false)
+  HLBM_DISPATCH(true, false, false, false)
+  HLBM_DISPATCH(true, false, true, false)
+  HLBM_DISPATCH(true, true, false, false)
+  HLBM_DISPATCH(true, true, true, false)
+  HLBM_DISPATCH(true, false, false, true)
+  HLBM_DISPATCH(true, false, true, true)
+  HLBM_DISPATCH(true, true, false, true)
+  HLBM_DISPATCH(true, true, true, true)
+#undef HLBM_DISPATCH
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hlbm

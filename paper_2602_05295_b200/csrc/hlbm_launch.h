@@ -1,0 +1,37 @@
+// Host-side launchers shared by the C-ABI translation unit.
+#pragma once
+#include "hlbm_params.cuh"
+
+namespace hlbm {
+
+struct Ranges {
+  double mn[10], mx[10];
+  double levels[10];
+};
+struct MaskGeo {
+  int nx, ny, nz;
+  int bc_ywall_lo, bc_ywall_hi, bc_zwall_lo, bc_zwall_hi;
+};
+
+cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
+                                  cudaStream_t st);
+cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
+                              int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st);
+cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
+                          const double* mom, const double* stress, int x0, int cnt,
+                          unsigned long long* sat, cudaStream_t st);
+cudaError_t launch_export(const Geo& g, const Ranges& R, bool q16, const void* src, double* rho,
+                          double* mom, double* stress, int x0, int cx, int y0, int cy, int z0, int cz,
+                          cudaStream_t st);
+cudaError_t launch_classify(const uint8_t* mask_ext, const MaskGeo& m, uint32_t* links, uint8_t* cls,
+                            cudaStream_t st);
+int64_t compact_tiles(int64_t n);
+cudaError_t launch_compact(const uint8_t* cls, const uint32_t* links, int64_t n, uint8_t want,
+                           int64_t* counts, int64_t* total, int64_t* out_cells, uint32_t* out_masks,
+                           bool count_only, cudaStream_t st);
+cudaError_t launch_special_bits(const uint8_t* cls, int nx, int ny, int nz, int row_words,
+                                uint32_t* bits, cudaStream_t st);
+cudaError_t launch_init_modes(const Geo& g, bool q16, const Ranges& R, void* dst, double rho0,
+                              const double* modes, int nmodes, cudaStream_t st);
+
+}  // namespace hlbm

@@ -1,0 +1,240 @@
+// Per-cell arithmetic of the HOME-LBM D3Q27 fluid step, shared by every kernel.
+//
+// Internal state per cell (fp32 path): d = rho - 1, j = rho*u (3), n = sneq (6, Voigt
+// xx,xy,xz,yy,yz,zz).  Populations are handled as deviations ft_i = f_i - w_i so that the
+// O(1) weights never enter a rounding (SURVEY.md §7 hard part 1).
+//
+// Reference formulas restated here (all under /root/reference/pkg/src/momentlbm/):
+//   collision    collide_moments 3D branch        collision.py:137-194 (tau = 0.5+3nu, :30-31)
+//   reconstruct  reconstruct_distributions        moments.py:64-90  (h2_contract, h3 labels
+//                                                  xxy,xyy,xxz,xzz,yzz,yyz,xyz each x 1/(2cs^6))
+//   extract      moments_from_distributions       moments.py:25-39
+//   neq split    neq_decompose / neq_recompose    moments.py:93-102
+// The reconstruction polynomial P(c) = f_i / w_i - 1 is expanded in monomials of c
+// (17 coefficients, see coeffs()) so that kernels can evaluate it by sum factorisation
+// using w_i = w1(cx) w1(cy) w1(cz), w1 = (1/6, 2/3, 1/6).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hlbm {
+
+// ------------------------------------------------------------------ packed f32x2 ops
+// Two lattice cells per thread: every arithmetic op below is one FADD2/FMUL2/FFMA2.
+typedef float2 V;
+__device__ __forceinline__ V vsplat(float s) { return make_float2(s, s); }
+__device__ __forceinline__ V vadd(V a, V b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ V vsub(V a, V b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ V vmul(V a, V b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ V vmul(V a, float s) { return __fmul2_rn(a, vsplat(s)); }
+__device__ __forceinline__ V vfma(V a, V b, V c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ V vfma(V a, float s, V c) { return __ffma2_rn(a, vsplat(s), c); }
+__device__ __forceinline__ V vneg(V a) { return make_float2(-a.x, -a.y); }
+
+// scalar overloads so templated code serves both the packed and the per-cell kernels
+__device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float vsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float vmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float vfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float vneg(float a) { return -a; }
+template <class T> __device__ __forceinline__ T splat(float s);
+template <> __device__ __forceinline__ float splat<float>(float s) { return s; }
+template <> __device__ __forceinline__ V splat<V>(float s) { return vsplat(s); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// one Newton step on top of MUFU.RCP: ~0.5 ulp, keeps 1/rho well inside the 1e-5 budget
+__device__ __forceinline__ float rcp_nr(float x) {
+  float r = rcp_approx(x);
+  float e = __fmaf_rn(-x, r, 1.0f);
+  return __fmaf_rn(r, e, r);
+}
+__device__ __forceinline__ V vrcp(V x) { return make_float2(rcp_nr(x.x), rcp_nr(x.y)); }
+__device__ __forceinline__ float vrcp(float x) { return rcp_nr(x); }
+
+// ------------------------------------------------------------------ relaxation constants
+struct Relax {
+  float om;     // 1 - s, s = 1/tau               (off-diagonal sneq factor, collision.py:189-191)
+  float cxy;    // (2 tau - 1)/(2 tau)           (collision.py:176)
+  float cd;     // (tau - 1)/(3 tau)             (collision.py:177)
+  float fx, fy, fz;  // uniform body force
+};
+
+// ------------------------------------------------------------------ reconstruction coefficients
+// P(c) - 1 (per unit weight) = K0 + L.c + sum_a Qaa c_a^2 + Qxy cx cy + Qxz cx cz + Qyz cy cz
+//        + Txxy cx^2 cy + Txyy cx cy^2 + Txxz cx^2 cz + Txzz cx cz^2 + Tyzz cy cz^2
+//        + Tyyz cy^2 cz + Txyz cx cy cz
+// All coefficients are pre-multiplied by 1/216 so that ft(c) = omega(cx)omega(cy)omega(cz) P
+// with omega(0) = 4, omega(+-1) = 1 (w1 = omega/6).
+template <class T>
+struct Coef {
+  T K0, Lx, Ly, Lz, Qxx, Qyy, Qzz, Qxy, Qxz, Qyz;
+  T Txxy, Txyy, Txxz, Txzz, Tyzz, Tyyz, Txyz;
+};
+
+// Post-collision (collision.py:137-194, written in sneq form) and expansion of the
+// third-order Hermite reconstruction (moments.py:64-90) for one (pair of) cell(s).
+//   X = rho S+  (full post-collision stress), Y = rho T (third-order closure, moments.py:42-52)
+template <class T, bool FORCE>
+__device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy,
+                                          T nyz, T nzz, const Relax& R) {
+  const T one = splat<T>(1.0f);
+  T rho = vadd(d, one);
+  T inv = vrcp(rho);
+  T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);   // pre-kick u (collision.py:158)
+  // diagonal: X_aa = j_a u_a + (1-s)(n_aa - tr n/3) [+ F_a u_a + cd(2F_a u_a - F_b u_b - F_g u_g)]
+  T q = vmul(vadd(vadd(nxx, nyy), nzz), splat<T>(1.0f / 3.0f));
+  const T om = splat<T>(R.om);
+  T Xxx = vfma(jx, ux, vmul(om, vsub(nxx, q)));
+  T Xyy = vfma(jy, uy, vmul(om, vsub(nyy, q)));
+  T Xzz = vfma(jz, uz, vmul(om, vsub(nzz, q)));
+  T Xxy = vfma(jx, uy, vmul(om, nxy));
+  T Xxz = vfma(jx, uz, vmul(om, nxz));
+  T Xyz = vfma(jy, uz, vmul(om, nyz));
+  T jpx = jx, jpy = jy, jpz = jz;
+  if (FORCE) {
+    const T fx = splat<T>(R.fx), fy = splat<T>(R.fy), fz = splat<T>(R.fz);
+    T fux = vmul(fx, ux), fuy = vmul(fy, uy), fuz = vmul(fz, uz);
+    const T cd = splat<T>(R.cd), cxy = splat<T>(R.cxy);
+    // F_a u_a + cd (2 F_a u_a - F_b u_b - F_g u_g)    (collision.py:183-186)
+    T sfu = vadd(vadd(fux, fuy), fuz);
+    T c1 = splat<T>(1.0f + 3.0f * R.cd);
+    Xxx = vadd(Xxx, vsub(vmul(c1, fux), vmul(cd, sfu)));
+    Xyy = vadd(Xyy, vsub(vmul(c1, fuy), vmul(cd, sfu)));
+    Xzz = vadd(Xzz, vsub(vmul(c1, fuz), vmul(cd, sfu)));
+    // cxy (F_a u_b + F_b u_a)                          (collision.py:189-191)
+    Xxy = vfma(cxy, vfma(fx, uy, vmul(fy, ux)), Xxy);
+    Xxz = vfma(cxy, vfma(fx, uz, vmul(fz, ux)), Xxz);
+    Xyz = vfma(cxy, vfma(fy, uz, vmul(fz, uy)), Xyz);
+    const T half = splat<T>(0.5f);
+    jpx = vfma(half, fx, jx);                      // mom + F/2 (collision.py:160)
+    jpy = vfma(half, fy, jy);
+    jpz = vfma(half, fz, jz);
+    ux = vmul(jpx, inv); uy = vmul(jpy, inv); uz = vmul(jpz, inv);   // u+ for the reconstruction
+  }
+  // Y_aab = X_aa u_b + 2 X_ab u_a - 2 j_a u_a u_b ;  Y_xyz = Xxy uz + Xxz uy + Xyz ux - 2 jx uy uz
+  const T two = splat<T>(2.0f);
+  T ax = vsub(Xxx, vmul(two, vmul(jpx, ux)));   // X_aa - 2 j_a u_a
+  T ay = vsub(Xyy, vmul(two, vmul(jpy, uy)));
+  T az = vsub(Xzz, vmul(two, vmul(jpz, uz)));
+  T Yxxy = vfma(ax, uy, vmul(two, vmul(Xxy, ux)));
+  T Yxyy = vfma(ay, ux, vmul(two, vmul(Xxy, uy)));
+  T Yxxz = vfma(ax, uz, vmul(two, vmul(Xxz, ux)));
+  T Yxzz = vfma(az, ux, vmul(two, vmul(Xxz, uz)));
+  T Yyzz = vfma(az, uy, vmul(two, vmul(Xyz, uz)));
+  T Yyyz = vfma(ay, uz, vmul(two, vmul(Xyz, uy)));
+  T Yxyz = vfma(Xxy, uz, vfma(Xxz, uy, vfma(Xyz, ux, vmul(splat<T>(-2.0f), vmul(jpx, vmul(uy, uz))))));
+  Coef<T> C;
+  // constant: d - (9/2)(1/3) tr X ; linear: 3 j - (27/2)(1/3)(Y..) ; /216 folded in
+  C.K0 = vfma(splat<T>(-1.5f / 216.0f), vadd(vadd(Xxx, Xyy), Xzz), vmul(d, splat<T>(1.0f / 216.0f)));
+  C.Lx = vfma(splat<T>(-4.5f / 216.0f), vadd(Yxyy, Yxzz), vmul(jpx, splat<T>(3.0f / 216.0f)));
+  C.Ly = vfma(splat<T>(-4.5f / 216.0f), vadd(Yxxy, Yyzz), vmul(jpy, splat<T>(3.0f / 216.0f)));
+  C.Lz = vfma(splat<T>(-4.5f / 216.0f), vadd(Yxxz, Yyyz), vmul(jpz, splat<T>(3.0f / 216.0f)));
+  const T q2 = splat<T>(4.5f / 216.0f), q11 = splat<T>(9.0f / 216.0f), t3 = splat<T>(13.5f / 216.0f);
+  C.Qxx = vmul(q2, Xxx); C.Qyy = vmul(q2, Xyy); C.Qzz = vmul(q2, Xzz);
+  C.Qxy = vmul(q11, Xxy); C.Qxz = vmul(q11, Xxz); C.Qyz = vmul(q11, Xyz);
+  C.Txxy = vmul(t3, Yxxy); C.Txyy = vmul(t3, Yxyy); C.Txxz = vmul(t3, Yxxz);
+  C.Txzz = vmul(t3, Yxzz); C.Tyzz = vmul(t3, Yyzz); C.Tyyz = vmul(t3, Yyyz);
+  C.Txyz = vmul(t3, Yxyz);
+  return C;
+}
+
+// ft_i for one compile-time direction (cx,cy,cz) and sign s = +1 (c) or -1 (-c):
+// returns omega(c) * P(s c)  (= 216 w_i P(s c) / 216 -> exactly ft_i).  Even/odd split:
+// P(+-c) = E(c) +- O(c).
+template <int cx, int cy, int cz, class T>
+__device__ __forceinline__ void eval_eo(const Coef<T>& C, T& E, T& O) {
+  // even part: K0 + Qaa c_a^2 + Qab c_a c_b
+  T e = C.K0;
+  if (cx) e = vadd(e, C.Qxx);
+  if (cy) e = vadd(e, C.Qyy);
+  if (cz) e = vadd(e, C.Qzz);
+  if (cx && cy) e = (cx * cy > 0) ? vadd(e, C.Qxy) : vsub(e, C.Qxy);
+  if (cx && cz) e = (cx * cz > 0) ? vadd(e, C.Qxz) : vsub(e, C.Qxz);
+  if (cy && cz) e = (cy * cz > 0) ? vadd(e, C.Qyz) : vsub(e, C.Qyz);
+  // odd part: L.c + third-order monomials (cubic in c)
+  T o = splat<T>(0.0f);
+  bool first = true;
+  auto acc = [&](int sgn, T v) {
+    if (first) { o = (sgn > 0) ? v : vneg(v); first = false; }
+    else o = (sgn > 0) ? vadd(o, v) : vsub(o, v);
+  };
+  if (cx) acc(cx, C.Lx);
+  if (cy) acc(cy, C.Ly);
+  if (cz) acc(cz, C.Lz);
+  if (cx && cy) { acc(cy, C.Txxy); acc(cx, C.Txyy); }   // cx^2 cy ; cx cy^2
+  if (cx && cz) { acc(cz, C.Txxz); acc(cx, C.Txzz); }
+  if (cy && cz) { acc(cy, C.Tyzz); acc(cz, C.Tyyz); }
+  if (cx && cy && cz) acc(cx * cy * cz, C.Txyz);
+  const float om = (cx ? 1.f : 4.f) * (cy ? 1.f : 4.f) * (cz ? 1.f : 4.f);
+  if (om != 1.f) { e = vmul(e, splat<T>(om)); o = first ? o : vmul(o, splat<T>(om)); }
+  E = e;
+  O = o;
+}
+
+// raw moments (of ft) -> stored state: d = m0, j = m1, n = (Pi~ - delta d/3) - j j / rho
+template <class T>
+__device__ __forceinline__ void raw_to_state(const T m[10], T out[10]) {
+  // m: [m000, m100, m010, m001, m200, m110, m101, m020, m011, m002]
+  T d = m[0];
+  T inv = vrcp(vadd(d, splat<T>(1.0f)));
+  T d3 = vmul(d, splat<T>(1.0f / 3.0f));
+  T jx = m[1], jy = m[2], jz = m[3];
+  T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);
+  out[0] = d;
+  out[1] = jx;
+  out[2] = jy;
+  out[3] = jz;
+  out[4] = vsub(vsub(m[4], d3), vmul(jx, ux));
+  out[5] = vsub(m[5], vmul(jx, uy));
+  out[6] = vsub(m[6], vmul(jx, uz));
+  out[7] = vsub(vsub(m[7], d3), vmul(jy, uy));
+  out[8] = vsub(m[8], vmul(jy, uz));
+  out[9] = vsub(vsub(m[9], d3), vmul(jz, uz));
+}
+
+// ------------------------------------------------------------------ 16-bit codec
+// decode: m = min + q * (max-min)/(2^b-1), evaluated as one FMA on the
+// exact float of q.  For component 0 the kernel decodes d = rho - 1 directly (min - 1).
+struct Codec {
+  float dec_step[10];   // (max-min)/(2^b-1)
+  float dec_off[10];    // min (component 0: min - 1)
+  float enc_scale[10];  // (2^b-1)/(max-min)
+  float enc_off[10];    // -min*scale + 1/2   (component 0: -(min-1)*scale + 1/2)
+  float sat_a[10];      // r = m*sat_a + sat_b, saturated iff |r| > 1
+  float sat_b[10];
+  uint32_t levels[10];  // 2^b - 1
+};
+
+__device__ __forceinline__ float code_lo_f(uint32_t w) {   // 2^23 + (w & 0xffff)
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7610));
+}
+__device__ __forceinline__ float code_hi_f(uint32_t w) {   // 2^23 + (w >> 16)
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7632));
+}
+
+// counter-based dither hash (oracle/codec.py: mix32 / dither_noise)
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+// 16 noise bits -> bits/65536 - 1/2 exactly: float(1 + bits/2^16) - 1.5
+__device__ __forceinline__ float noise16(uint32_t bits16) {
+  return __uint_as_float(0x3F800000u | (bits16 << 7)) - 1.5f;
+}
+
+// floor, saturating to [0, 2^32-1] (negative and NaN -> 0); callers clamp to 2^b - 1
+__device__ __forceinline__ uint32_t f2u16_floor(float t) {
+  uint32_t r;
+  asm("cvt.rmi.u32.f32 %0, %1;" : "=r"(r) : "f"(t));
+  return r;
+}
+
+}  // namespace hlbm

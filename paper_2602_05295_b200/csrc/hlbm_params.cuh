@@ -1,0 +1,57 @@
+// Kernel-side parameter blocks and HBM layout of the slab state.
+//
+// Layout: one allocation per buffer, x-plane major so that an x-plane
+// holding every component is contiguous (halo planes ship without packing):
+//     state[xs][c][y][z],   xs = 0 .. nx+1  (xs = 0 and nx+1 are ghost planes)
+//   fp32: c = 0..9  -> d = rho-1, j_x, j_y, j_z, sneq_xx, xy, xz, yy, yz, zz   (float)
+//   q16 : c = 0..4  -> u32 words, word k = code(2k) | code(2k+1) << 16
+#pragma once
+#include <stdint.h>
+#include "hlbm_math.cuh"
+
+namespace hlbm {
+
+constexpr int kNW = 16;          // warps per CTA = y rows held by a CTA (14 interior + 2 halo)
+constexpr int kRows = kNW - 2;   // interior rows per CTA
+constexpr int kZW = 64;          // z cells covered by one warp (32 lanes x 2 cells)
+constexpr int kZT = 60;          // interior z cells per tile (window start stays 16 B aligned)
+constexpr int kNSlot = 18;       // exchanged values per cell pair: (cx 3) x (cy +-1) x (kz 3)
+
+struct Geo {
+  int nx, ny, nz;          // local interior dims (x = slab axis)
+  int64_t cstride;         // ny*nz            elements between components
+  int64_t pstride;         // NC*ny*nz         elements between x planes
+  int x_lo_src, x_hi_src;  // storage plane read for source plane -1 / nx ; -1 => inflow constants
+  int nzt, nyt, nxs, xseg; // tiling of the interior kernel
+  int gx0, gny, gnz;       // slab offset in the global grid (dither key)
+  int gnx_total;           // global nx
+};
+
+struct Stats {                 // device-side accumulators (reset by the host per step batch)
+  double mass_dev;             // sum over fluid cells of (rho - 1)
+  double mom[3];
+  unsigned int max_u2_bits;    // float bits of max |u|^2 (NaN sorts above +inf)
+  unsigned int nonfinite;
+  unsigned long long sat[10];
+};
+
+struct StepArgs {
+  const void* in;
+  void* out;
+  Geo g;
+  Relax R;
+  Codec Q;
+  float inflow[10];                 // internal-form state of an inflow ghost plane
+  const uint32_t* special_bits;     // per (xs,y) row bitmask of boundary/solid cells, or null
+  int bits_row_words;               // u32 words per bitmask row
+  uint32_t step_key;                // dither key for this step
+  int do_stats;
+  Stats* stats;
+};
+
+__host__ __device__ __forceinline__ int wrapi(int a, int n) {
+  a %= n;
+  return a < 0 ? a + n : a;
+}
+
+}  // namespace hlbm

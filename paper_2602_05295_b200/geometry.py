@@ -1,0 +1,127 @@
+"""Voxel solid masks for the benchmark scenes (input construction, host side).
+
+The split scheme's boundary handling works on a voxel solid mask (the north-star variant of
+the paper's surface voxelization).  These builders make
+the masks of SURVEY.md §8(d) configs 3-5; the boundary lists and link masks are built on
+the GPU by ``Solver.set_mask`` (csrc/hlbm_cells.cu).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def sphere_mask(dims, center, radius) -> np.ndarray:
+    """Cells whose centre lies inside the sphere (voxel test at cell centres)."""
+    nx, ny, nz = dims
+    x = np.arange(nx)[:, None, None] - center[0]
+    y = np.arange(ny)[None, :, None] - center[1]
+    z = np.arange(nz)[None, None, :] - center[2]
+    return ((x * x + y * y + z * z) <= radius * radius).astype(np.uint8)
+
+
+def _box(m, lo, hi):
+    nx, ny, nz = m.shape
+    a = [max(0, int(round(l))) for l in lo]
+    b = [min(n, int(round(h))) for h, n in zip(hi, (nx, ny, nz))]
+    if all(bb > aa for aa, bb in zip(a, b)):
+        m[a[0]:b[0], a[1]:b[1], a[2]:b[2]] = 1
+
+
+def _ellipsoid(m, c, r):
+    nx, ny, nz = m.shape
+    x0, x1 = max(0, int(c[0] - r[0]) - 1), min(nx, int(c[0] + r[0]) + 2)
+    y0, y1 = max(0, int(c[1] - r[1]) - 1), min(ny, int(c[1] + r[1]) + 2)
+    z0, z1 = max(0, int(c[2] - r[2]) - 1), min(nz, int(c[2] + r[2]) + 2)
+    x = (np.arange(x0, x1)[:, None, None] - c[0]) / r[0]
+    y = (np.arange(y0, y1)[None, :, None] - c[1]) / r[1]
+    z = (np.arange(z0, z1)[None, None, :] - c[2]) / r[2]
+    m[x0:x1, y0:y1, z0:z1] |= ((x * x + y * y + z * z) <= 1.0).astype(np.uint8)
+
+
+def _cylinder_y(m, c, radius, y0, y1):
+    """Cylinder with axis along y (a wheel), centre (cx, cz)."""
+    nx, ny, nz = m.shape
+    xa, xb = max(0, int(c[0] - radius) - 1), min(nx, int(c[0] + radius) + 2)
+    za, zb = max(0, int(c[1] - radius) - 1), min(nz, int(c[1] + radius) + 2)
+    x = np.arange(xa, xb)[:, None] - c[0]
+    z = np.arange(za, zb)[None, :] - c[1]
+    disk = (x * x + z * z) <= radius * radius
+    ya, yb = max(0, int(y0)), min(ny, int(y1))
+    if yb > ya:
+        m[xa:xb, ya:yb, za:zb] |= disk[:, None, :].astype(np.uint8)
+
+
+def vehicle_mask(dims, seed=0) -> np.ndarray:
+    """Seeded procedural vehicle-like obstacle (body, cabin, 4 wheels, rear wing).
+
+    Coordinates: x streamwise, y spanwise, z vertical; the car sits on z = 0 and occupies a
+    few percent of the domain."""
+    nx, ny, nz = dims
+    rng = np.random.default_rng(seed)
+    m = np.zeros(dims, dtype=np.uint8)
+    L = 0.40 * nx * (1 + 0.05 * rng.uniform(-1, 1))
+    W = 0.36 * ny * (1 + 0.05 * rng.uniform(-1, 1))
+    H = 0.16 * nz * (1 + 0.05 * rng.uniform(-1, 1))
+    x0 = 0.22 * nx
+    yc = ny / 2
+    clearance = 0.04 * nz
+    wheel_r = 0.07 * nz
+    # body: box + rounded nose / tail
+    _box(m, (x0, yc - W / 2, clearance + wheel_r * 0.6), (x0 + L, yc + W / 2, clearance + wheel_r * 0.6 + H))
+    _ellipsoid(m, (x0, yc, clearance + wheel_r * 0.6 + H / 2), (0.10 * L, W / 2, H / 2))
+    _ellipsoid(m, (x0 + L, yc, clearance + wheel_r * 0.6 + H / 2), (0.06 * L, W / 2, H / 2))
+    # cabin
+    _ellipsoid(m, (x0 + 0.55 * L, yc, clearance + wheel_r * 0.6 + H), (0.25 * L, 0.40 * W, 0.55 * H))
+    # wheels
+    for fx in (0.18, 0.80):
+        for side in (-1, 1):
+            ya = yc + side * (W / 2) - (0.12 * W if side > 0 else 0.0)
+            _cylinder_y(m, (x0 + fx * L, wheel_r), wheel_r, ya, ya + 0.12 * W)
+    # rear wing on two struts
+    zw = clearance + wheel_r * 0.6 + 1.7 * H
+    _box(m, (x0 + 0.92 * L, yc - 0.45 * W, zw), (x0 + 1.02 * L, yc + 0.45 * W, zw + 0.05 * nz))
+    for s in (-0.25, 0.25):
+        _box(m, (x0 + 0.95 * L, yc + s * W - 1, clearance + wheel_r * 0.6 + H), (x0 + 0.97 * L, yc + s * W + 1, zw))
+    return m
+
+
+def turbulence_modes(n, kmin=1.0, kmax=4.0, u_rms=0.05, seed=0, dims=None) -> np.ndarray:
+    """Solenoidal random Fourier modes (kx,ky,kz, ax,ay,az, phase) with kmin <= |k| <= kmax,
+    scaled so that the velocity field has the requested rms."""
+    rng = np.random.default_rng(seed)
+    kr = int(np.ceil(kmax))
+    modes = []
+    for kx in range(-kr, kr + 1):
+        for ky in range(-kr, kr + 1):
+            for kz in range(0, kr + 1):
+                if kz == 0 and (ky < 0 or (ky == 0 and kx <= 0)):
+                    continue   # one of each +-k pair
+                k = np.array([kx, ky, kz], dtype=np.float64)
+                kn = np.linalg.norm(k)
+                if kn < kmin or kn > kmax:
+                    continue
+                a = rng.normal(size=3)
+                a -= k * (a @ k) / (kn * kn)          # solenoidal: a . k = 0
+                a *= kn ** (-5.0 / 6.0)               # mild spectral slope
+                modes.append([kx, ky, kz, a[0], a[1], a[2], rng.uniform(0, 2 * np.pi)])
+    modes = np.array(modes, dtype=np.float64)
+    # each mode contributes <sin^2> = 1/2 of |a|^2 to <|u|^2>; rms over 3 components
+    e = 0.5 * np.sum(modes[:, 3:6] ** 2)
+    modes[:, 3:6] *= u_rms * np.sqrt(3.0 / (2.0 * e)) if e > 0 else 0.0
+    return modes
+
+
+def evaluate_modes(modes, shape, origin=(0, 0, 0), global_dims=None):
+    """Host evaluation of the mode sum on a box (used by tests to build oracle inputs)."""
+    gd = global_dims if global_dims is not None else shape
+    x = (np.arange(shape[0]) + origin[0])[:, None, None] / gd[0]
+    y = (np.arange(shape[1]) + origin[1])[None, :, None] / gd[1]
+    z = (np.arange(shape[2]) + origin[2])[None, None, :] / gd[2]
+    u = np.zeros((3,) + tuple(shape))
+    for kx, ky, kz, ax, ay, az, ph in modes:
+        s = np.sin(2 * np.pi * (kx * x + ky * y + kz * z) + ph)
+        u[0] += ax * s
+        u[1] += ay * s
+        u[2] += az * s
+    return u
