@@ -1,4 +1,6 @@
 // C-ABI implementation: context, buffers, stepping (host side of include/hlbm.h).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +23,8 @@ struct hlbm_ctx {
   bool own_stream = false;
   size_t elem_bytes = 4;
   int64_t plane_elems = 0, total_elems = 0;
+  int zp = 0;
+  CUtensorMap tmap[2];
   void* buf[2] = {nullptr, nullptr};
   int cur = 0;
   Stats* d_stats = nullptr;
@@ -62,7 +66,8 @@ Geo make_geo(const hlbm_ctx* ctx) {
   const hlbm_config& c = ctx->cfg;
   Geo g{};
   g.nx = c.nx; g.ny = c.ny; g.nz = c.nz;
-  g.cstride = (int64_t)c.ny * c.nz;
+  g.zp = ctx->zp;
+  g.cstride = (int64_t)(c.ny + 2) * ctx->zp;
   g.pstride = ctx->plane_elems;
   g.x_lo_src = ctx->x_lo_src;
   g.x_hi_src = ctx->x_hi_src;
@@ -83,6 +88,7 @@ uint32_t step_key(int64_t step, uint32_t seed) {   // oracle/codec.py: step_key
 
 StepArgs make_args(hlbm_ctx* ctx, int with_stats) {
   StepArgs A{};
+  A.tmap_in = ctx->tmap[ctx->cur];
   A.in = ctx->buf[ctx->cur];
   A.out = ctx->buf[1 - ctx->cur];
   A.g = make_geo(ctx);
@@ -99,6 +105,29 @@ StepArgs make_args(hlbm_ctx* ctx, int with_stats) {
 
 unsigned long long* sat_ptr(hlbm_ctx* ctx) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->d_stats) + offsetof(Stats, sat));
+}
+
+// 4-D tensor map (zs, ys, c, xs) over one state buffer; box = one CTA plane tile
+int make_tensor_map(hlbm_ctx* ctx, int b) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return fail(ctx, HLBM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const hlbm_config& c = ctx->cfg;
+  cuuint64_t dims[4] = {(cuuint64_t)ctx->zp, (cuuint64_t)(c.ny + 2), (cuuint64_t)ctx->NC, (cuuint64_t)(c.nx + 2)};
+  cuuint64_t strides[3] = {(cuuint64_t)ctx->zp * 4, (cuuint64_t)(c.ny + 2) * ctx->zp * 4,
+                           (cuuint64_t)ctx->plane_elems * 4};
+  cuuint32_t box[4] = {(cuuint32_t)kZW, (cuuint32_t)kNW, (cuuint32_t)ctx->NC, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode(&ctx->tmap[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, ctx->buf[b], dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, HLBM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return HLBM_OK;
 }
 
 bool has_force(const hlbm_ctx* ctx) {
@@ -197,7 +226,8 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
   else ctx->x_hi_src = nx;
 
   ctx->elem_bytes = 4;
-  ctx->plane_elems = (int64_t)ctx->NC * c.ny * c.nz;
+  ctx->zp = (c.nz + 2 + 3) / 4 * 4;
+  ctx->plane_elems = (int64_t)ctx->NC * (c.ny + 2) * ctx->zp;
   ctx->total_elems = ctx->plane_elems * (nx + 2);
   *out = ctx;
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -205,13 +235,16 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
   for (int b = 0; b < 2; ++b) {
     CK(cudaMalloc(&ctx->buf[b], ctx->total_elems * 4));
     CK(cudaMemset(ctx->buf[b], 0, ctx->total_elems * 4));
+    if (int r = make_tensor_map(ctx, b)) return r;
   }
   CK(cudaMalloc(&ctx->d_stats, sizeof(Stats)));
   CK(cudaMemset(ctx->d_stats, 0, sizeof(Stats)));
   for (int i = 0; i < 3; ++i) CK(cudaEventCreate(&ctx->ev[i]));
   // default state: rest (rho = 1, j = 0, sneq = 0) in both buffers
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 2; ++b) {
     CK(launch_init_modes(make_geo(ctx), ctx->q16, ctx->RG, ctx->buf[b], 1.0, nullptr, 0, ctx->stream));
+    CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[b], ctx->stream));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   return HLBM_OK;
 }
@@ -289,6 +322,8 @@ int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const 
                      sat_ptr(ctx), ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
+  CK(launch_fill_ghosts(g, ctx->NC, ctx->buf[ctx->cur], ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(dr);
   cudaFree(dm);
   cudaFree(ds);
@@ -342,6 +377,7 @@ int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmo
   }
   CK(launch_init_modes(make_geo(ctx), ctx->q16, ctx->RG, ctx->buf[ctx->cur], rho0, dmodes, nmodes,
                        ctx->stream));
+  CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(dmodes);
   return HLBM_OK;
@@ -351,15 +387,13 @@ int hlbm_get_codes(hlbm_ctx* ctx, uint32_t* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
   if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
   const hlbm_config& c = ctx->cfg;
-  const int64_t pl = (int64_t)c.ny * c.nz, n = pl * c.nx;
-  // device [x][k][y][z] -> host [k][x][y][z]
-  CK(cudaMemcpy2DAsync(words, pl * 4, (char*)ctx->buf[ctx->cur] + ctx->plane_elems * 4, ctx->plane_elems * 4,
-                       pl * 4, c.nx, cudaMemcpyDeviceToHost, ctx->stream));
-  for (int k = 1; k < 5; ++k)
-    CK(cudaMemcpy2DAsync(words + k * n, pl * 4,
-                         (char*)ctx->buf[ctx->cur] + ctx->plane_elems * 4 + k * pl * 4,
-                         ctx->plane_elems * 4, pl * 4, c.nx, cudaMemcpyDeviceToHost, ctx->stream));
+  const int64_t n = (int64_t)5 * c.nx * c.ny * c.nz;
+  uint32_t* d = nullptr;
+  CK(cudaMalloc(&d, n * 4));
+  CK(launch_pack_codes(make_geo(ctx), ctx->buf[ctx->cur], d, 0, ctx->stream));
+  CK(cudaMemcpyAsync(words, d, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d);
   return HLBM_OK;
 }
 
@@ -367,11 +401,14 @@ int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
   if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
   const hlbm_config& c = ctx->cfg;
-  const int64_t pl = (int64_t)c.ny * c.nz, n = pl * c.nx;
-  for (int k = 0; k < 5; ++k)
-    CK(cudaMemcpy2DAsync((char*)ctx->buf[ctx->cur] + ctx->plane_elems * 4 + k * pl * 4, ctx->plane_elems * 4,
-                         words + k * n, pl * 4, pl * 4, c.nx, cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t n = (int64_t)5 * c.nx * c.ny * c.nz;
+  uint32_t* d = nullptr;
+  CK(cudaMalloc(&d, n * 4));
+  CK(cudaMemcpyAsync(d, words, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_pack_codes(make_geo(ctx), ctx->buf[ctx->cur], d, 1, ctx->stream));
+  CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d);
   return HLBM_OK;
 }
 

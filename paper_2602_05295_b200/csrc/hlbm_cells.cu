@@ -33,7 +33,7 @@ __device__ __forceinline__ void load_cell(const StepArgs& A, int sp, int y, int 
     for (int c = 0; c < 10; ++c) s[c] = A.inflow[c];
     return;
   }
-  const int64_t off = (int64_t)sp * g.pstride + (int64_t)y * g.nz + z;
+  const int64_t off = cell_off(g, sp, y, z);   // y, z may be -1 / n: ghost images
   if (!Q16) {
     const float* p = reinterpret_cast<const float*>(A.in) + off;
 #pragma unroll
@@ -57,8 +57,8 @@ __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z
   const Geo& g = A.g;
   const bool bb = (mask >> I) & 1u;
   const int sx = bb ? x : x - cx;
-  const int sy = bb ? y : wrapi(y - cy, g.ny);
-  const int sz = bb ? z : wrapi(z - cz, g.nz);
+  const int sy = bb ? y : y - cy;   // ghost rows/columns hold the periodic images
+  const int sz = bb ? z : z - cz;
   float s[10];
   load_cell<Q16>(A, src_plane(g, sx), sy, sz, s);
   const Coef<float> C = coeffs<float, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
@@ -90,15 +90,26 @@ struct PullAll<27, Q16, FORCE> {
   __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*) {}
 };
 
+template <typename E>
+__device__ __forceinline__ void put_cell(const Geo& g, E* plane, int y, int z, const E* v, int ncomp) {
+  // the cell and, at y/z edges, its periodic images in the ghost layers
+  const int yi = y == 0 ? g.ny : (y == g.ny - 1 ? -1 : y);
+  const int zi = z == 0 ? g.nz : (z == g.nz - 1 ? -1 : z);
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      if ((a && yi == y) || (b && zi == z)) continue;
+      E* p = plane + (int64_t)((a ? yi : y) + 1) * g.zp + ((b ? zi : z) + 1);
+      for (int c = 0; c < ncomp; ++c) p[c * g.cstride] = v[c];
+    }
+}
+
 template <bool Q16, bool DITHER>
 __device__ __forceinline__ void store_cell(const StepArgs& A, int x, int y, int z, const float s[10],
                                            bool stat, float red[5]) {
   const Geo& g = A.g;
-  const int64_t off = (int64_t)(x + 1) * g.pstride + (int64_t)y * g.nz + z;
+  const int64_t plane_off = (int64_t)(x + 1) * g.pstride;
   if (!Q16) {
-    float* p = reinterpret_cast<float*>(A.out) + off;
-#pragma unroll
-    for (int c = 0; c < 10; ++c) p[c * g.cstride] = s[c];
+    put_cell(g, reinterpret_cast<float*>(A.out) + plane_off, y, z, s, 10);
   } else {
     float nz[10];
     if (DITHER) {
@@ -112,22 +123,18 @@ __device__ __forceinline__ void store_cell(const StepArgs& A, int x, int y, int 
       }
     }
     uint32_t code[10];
-    bool any_sat = false;
 #pragma unroll
     for (int c = 0; c < 10; ++c) {
       float t = __fmaf_rn(s[c], A.Q.enc_scale[c], A.Q.enc_off[c]);
       if (DITHER) t += nz[c];
       code[c] = min(f2u16_floor(t), A.Q.levels[c]);
       const float r = __fmaf_rn(s[c], A.Q.sat_a[c], A.Q.sat_b[c]);
-      if (stat && !(fabsf(r) <= 1.0f)) {
-        atomicAdd(&A.stats->sat[c], 1ull);
-        any_sat = true;
-      }
+      if (stat && !(fabsf(r) <= 1.0f)) atomicAdd(&A.stats->sat[c], 1ull);
     }
-    (void)any_sat;
-    uint32_t* p = reinterpret_cast<uint32_t*>(A.out) + off;
+    uint32_t wd[5];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) p[k * g.cstride] = __byte_perm(code[2 * k], code[2 * k + 1], 0x5410);
+    for (int k = 0; k < 5; ++k) wd[k] = __byte_perm(code[2 * k], code[2 * k + 1], 0x5410);
+    put_cell(g, reinterpret_cast<uint32_t*>(A.out) + plane_off, y, z, wd, 5);
   }
   if (stat) {
     red[0] += s[0]; red[1] += s[1]; red[2] += s[2]; red[3] += s[3];
@@ -372,7 +379,8 @@ __global__ void import_f64(Geo g, Ranges R, void* dst, const double* __restrict_
                           stress[3 * n + i] - j1 * j1 / rh,
                           stress[4 * n + i] - j1 * j2 / rh,
                           stress[5 * n + i] - j2 * j2 / rh};
-    const int64_t off = (int64_t)(x0 + xl + 1) * g.pstride + r;
+    const int yy = (int)(r / g.nz), zz = (int)(r - (int64_t)yy * g.nz);
+    const int64_t off = cell_off(g, x0 + xl + 1, yy, zz);
     if (!Q16) {
       float* p = reinterpret_cast<float*>(dst) + off;
       p[0] = (float)(rh - 1.0);
@@ -405,7 +413,7 @@ __global__ void export_f64(Geo g, Ranges R, const void* src, double* __restrict_
     const int64_t r = i - (int64_t)xl * cy * cz;
     const int yl = (int)(r / cz), zl = (int)(r - (int64_t)yl * cz);
     const int y = wrapi(y0 + yl, g.ny), z = wrapi(z0 + zl, g.nz);
-    const int64_t off = (int64_t)(x0 + xl + 1) * g.pstride + (int64_t)y * g.nz + z;
+    const int64_t off = cell_off(g, x0 + xl + 1, y, z);
     double v[10];
     if (!Q16) {
       const float* p = reinterpret_cast<const float*>(src) + off;
@@ -460,7 +468,7 @@ __global__ void init_modes(Geo g, Ranges R, void* dst, double rho0, const double
       u[2] += md[5] * sn;
     }
     const double v[10] = {rho0, rho0 * u[0], rho0 * u[1], rho0 * u[2], 0, 0, 0, 0, 0, 0};
-    const int64_t off = (int64_t)(x + 1) * g.pstride + r;
+    const int64_t off = cell_off(g, x + 1, y, z);
     if (!Q16) {
       float* p = reinterpret_cast<float*>(dst) + off;
       p[0] = (float)(rho0 - 1.0);
@@ -475,6 +483,52 @@ __global__ void init_modes(Geo g, Ranges R, void* dst, double rho0, const double
       uint32_t* p = reinterpret_cast<uint32_t*>(dst) + off;
       for (int k = 0; k < 5; ++k) p[k * g.cstride] = code[2 * k] | (code[2 * k + 1] << 16);
     }
+  }
+}
+
+// copy edge columns of every interior row into the z ghost columns (periodic images)
+__global__ void fill_ghosts(Geo g, int NC, uint32_t* buf) {
+  const int64_t n = (int64_t)g.nx * NC * 2 * g.ny;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pc = i / (2 * g.ny);
+    const int k = (int)(i - pc * 2 * g.ny);
+    const int x = (int)(pc / NC), c = (int)(pc - (int64_t)x * NC);
+    uint32_t* row = buf + (int64_t)(x + 1) * g.pstride + (int64_t)c * g.cstride + (int64_t)((k >> 1) + 1) * g.zp;
+    if (k & 1) row[g.nz + 1] = row[1];
+    else row[0] = row[g.nz];
+  }
+}
+
+// ghost rows (after the columns are filled, so corners are consistent)
+__global__ void fill_ghost_rows(Geo g, int NC, uint32_t* buf) {
+  const int rowsz = g.nz + 2;
+  const int64_t n = (int64_t)g.nx * NC * 2 * rowsz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pc = i / (2 * rowsz);
+    const int k = (int)(i - pc * 2 * rowsz);
+    const int x = (int)(pc / NC), c = (int)(pc - (int64_t)x * NC);
+    uint32_t* base = buf + (int64_t)(x + 1) * g.pstride + (int64_t)c * g.cstride;
+    const int zz = k >> 1;
+    if (k & 1) base[(int64_t)(g.ny + 1) * g.zp + zz] = base[(int64_t)1 * g.zp + zz];
+    else base[zz] = base[(int64_t)g.ny * g.zp + zz];
+  }
+}
+
+// interior words of the q16 state <-> dense (5, nx, ny, nz)
+__global__ void pack_codes(Geo g, const uint32_t* __restrict__ buf, uint32_t* __restrict__ dense, int dir) {
+  const int64_t nc = (int64_t)g.nx * g.ny * g.nz, n = 5 * nc;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / nc);
+    const int64_t cell = i - (int64_t)k * nc;
+    const int x = (int)(cell / ((int64_t)g.ny * g.nz));
+    const int64_t r = cell - (int64_t)x * g.ny * g.nz;
+    const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
+    const int64_t off = cell_off(g, x + 1, y, z) + (int64_t)k * g.cstride;
+    if (dir == 0) dense[i] = buf[off];
+    else const_cast<uint32_t*>(buf)[off] = dense[i];
   }
 }
 
@@ -507,6 +561,20 @@ cudaError_t launch_export(const Geo& g, const Ranges& R, bool q16, const void* s
   const int64_t n = (int64_t)cx * cy * cz;
   if (q16) export_f64<true><<<grid_for(n, 256), 256, 0, st>>>(g, R, src, rho, mom, stress, x0, cx, y0, cy, z0, cz);
   else export_f64<false><<<grid_for(n, 256), 256, 0, st>>>(g, R, src, rho, mom, stress, x0, cx, y0, cy, z0, cz);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_ghosts(const Geo& g, int NC, void* buf, cudaStream_t st) {
+  const int64_t n1 = (int64_t)g.nx * NC * 2 * g.ny;
+  fill_ghosts<<<grid_for(n1, 256), 256, 0, st>>>(g, NC, reinterpret_cast<uint32_t*>(buf));
+  const int64_t n2 = (int64_t)g.nx * NC * 2 * (g.nz + 2);
+  fill_ghost_rows<<<grid_for(n2, 256), 256, 0, st>>>(g, NC, reinterpret_cast<uint32_t*>(buf));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_codes(const Geo& g, void* buf, uint32_t* dense, int dir, cudaStream_t st) {
+  const int64_t n = (int64_t)5 * g.nx * g.ny * g.nz;
+  pack_codes<<<grid_for(n, 256), 256, 0, st>>>(g, reinterpret_cast<uint32_t*>(buf), dense, dir);
   return cudaGetLastError();
 }
 

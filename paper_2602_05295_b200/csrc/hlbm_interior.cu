@@ -9,14 +9,15 @@
 // Mapping:
 //   * CTA = 16 warps; warp w holds y row (y0 - 1 + w); rows 1..14 are written, rows 0/15 are
 //     halo rows that only produce the populations their neighbour needs.
-//   * lane l holds the z pair (zb + 2l, zb + 2l + 1); every arithmetic op is packed f32x2
-//     (FFMA2/FADD2/FMUL2).  Cells zb+1 .. zb+60 are written.
+//   * lane l holds the z pair at storage columns (zs0 + 2l, zs0 + 2l + 1); every arithmetic op
+//     is packed f32x2 (FFMA2/FADD2/FMUL2).  Columns zs0+1 .. zs0+60 are written.
 //   * the CTA marches along x over a segment; the x-direction of streaming is a register
 //     rotation (two 10-moment accumulators), never a memory exchange.
 //   * streaming is sum-factorised by axis: z shifts are warp shuffles, y shifts exchange 18
 //     f32x2 per lane through shared memory, x shifts are the marching accumulators.
-//   * input planes are staged into shared memory by 1-D bulk TMA copies (cp.async.bulk +
-//     mbarrier), STAGES planes ahead of the consumer.
+//   * each input plane tile (64 z x 16 y x NC components) is ONE 4-D tensor TMA copy
+//     (cp.async.bulk.tensor + mbarrier) into shared memory, STAGES planes ahead; the y/z ghost
+//     layers of the layout make every tile in-bounds (no wrap).
 #include "hlbm_params.cuh"
 
 namespace hlbm {
@@ -41,11 +42,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -71,36 +73,19 @@ struct Smem {
   float red[kNW][5];
 };
 
-// Producer: warp 0 issues the bulk copies of source plane p into one stage.
+// Producer (one thread): the whole plane tile of source plane p is one tensor copy.
 template <int NC>
 __device__ __forceinline__ void issue_plane(const StepArgs& A, int p, uint32_t (*stage)[kNW][kZW],
-                                            uint64_t* bar, int zb, int y0, int lane) {
+                                            uint64_t* bar, int zs0, int ys0) {
   const Geo& g = A.g;
-  int sp;
-  if (p < 0) sp = g.x_lo_src;
-  else if (p >= g.nx) sp = g.x_hi_src;
-  else sp = p + 1;
-  const bool inflow = sp < 0;
-  if (lane == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive_expect_tx(bar, inflow ? 0u : (uint32_t)(NC * kNW * kZW * 4));
+  const int sp = (p < 0) ? g.x_lo_src : (p >= g.nx ? g.x_hi_src : p + 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (sp < 0) {   // inflow ghost plane: constants, nothing to load
+    mbar_arrive_expect_tx(bar, 0u);
+    return;
   }
-  __syncwarp();
-  if (inflow) return;
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(A.in) + (int64_t)sp * g.pstride;
-  for (int r = lane; r < NC * kNW; r += 32) {
-    const int c = r / kNW, w = r - c * kNW;
-    const int y = wrapi(y0 - 1 + w, g.ny);
-    const uint32_t* row = base + c * g.cstride + (int64_t)y * g.nz;
-    uint32_t* dst = stage[c][w];
-    int z = zb, done = 0;
-    while (done < kZW) {
-      const int n = min(kZW - done, g.nz - z);
-      bulk_g2s(dst + done, row + z, (uint32_t)n * 4u, bar);
-      done += n;
-      z = 0;
-    }
-  }
+  mbar_arrive_expect_tx(bar, (uint32_t)(NC * kNW * kZW * 4));
+  tma_load_4d(&stage[0][0][0], &A.tmap_in, zs0, ys0, 0, sp, bar);
 }
 
 // Partial moments of one destination plane.  Index order of the 6 "kx=0" moments:
@@ -120,8 +105,8 @@ struct Part6 {   // only the cx=+1 contribution of source q-1: kx=1/kx=2 partial
 // results to shared memory; returns the cy = 0 results g[kz] (added to the x accumulators
 // before the barrier so nothing but the accumulators is live across it).
 template <int CX>
-__device__ __forceinline__ void recon_cx(const Coef<V>& C, bool need_p, bool need_0, bool need_m,
-                                         V (*exch)[kNW][32], int w, int lane, V g0out[3]) {
+__device__ __forceinline__ void recon_cx(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane,
+                                         V g0out[3]) {
   V G00, G10, G20, G01, G11, G21, G02, G12;
   if (CX == 0) {
     const float f4 = 4.0f;
@@ -142,9 +127,6 @@ __device__ __forceinline__ void recon_cx(const Coef<V>& C, bool need_p, bool nee
 #pragma unroll
   for (int cyi = 0; cyi < 3; ++cyi) {
     const int CY = (cyi == 0) ? 1 : (cyi == 1 ? -1 : 0);   // +1, -1, then 0
-    if (CY > 0 && !need_p) continue;
-    if (CY < 0 && !need_m) continue;
-    if (CY == 0 && !need_0) continue;
     V B0, B1, B2;
     if (CY == 0) {
       B0 = vmul(G00, 4.0f); B1 = vmul(G01, 4.0f); B2 = vmul(G02, 4.0f);
@@ -211,29 +193,60 @@ __device__ __forceinline__ void load_state(const uint32_t (*st)[kNW][kZW], int w
   }
 }
 
-// store of one finished cell pair + fused statistics
+// image writes of an edge cell into the y/z ghost layers (periodic images; harmless for walls)
+template <typename E>
+__device__ __forceinline__ void write_images(const Geo& g, E* base_plane, int y, int z, const E* vals,
+                                             int ncomp) {
+  const int ys[2] = {y, y == 0 ? g.ny : (y == g.ny - 1 ? -1 : y)};
+  const int zs[2] = {z, z == 0 ? g.nz : (z == g.nz - 1 ? -1 : z)};
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      if (a == 0 && b == 0) continue;
+      if ((a && ys[1] == y) || (b && zs[1] == z)) continue;
+      E* p = base_plane + (int64_t)(ys[a] + 1) * g.zp + (zs[b] + 1);
+      for (int c = 0; c < ncomp; ++c) p[c * g.cstride] = vals[c];
+    }
+}
+
+// store of one finished cell pair + fused statistics.  zs = storage column of the .x cell
+// (even -> 8-byte aligned pair); logical z of .x is zs - 1.
 template <bool Q16, bool DITHER>
-__device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z0,
+__device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int zs,
                                            bool wx, bool wy, bool statx, bool staty, float red[5]) {
   const Geo& g = A.g;
   V s[10];
   raw_to_state(m, s);
-  const int64_t off = (int64_t)(q + 1) * g.pstride + (int64_t)y * g.nz + z0;
+  const int64_t plane_off = (int64_t)(q + 1) * g.pstride;
+  const int64_t off = plane_off + (int64_t)(y + 1) * g.zp + zs;
+  const int zx = zs - 1, zy = zs;
+  const bool edge = (y == 0) || (y == g.ny - 1) || (wx && (zx == 0 || zx == g.nz - 1)) ||
+                    (wy && (zy == 0 || zy == g.nz - 1));
   if (!Q16) {
     float* out = reinterpret_cast<float*>(A.out) + off;
+    if (wx && wy) {
 #pragma unroll
-    for (int c = 0; c < 10; ++c) {
-      float* p = out + c * g.cstride;
-      if (wx && wy) *reinterpret_cast<V*>(p) = s[c];
-      else if (wx) p[0] = s[c].x;
-      else if (wy) p[1] = s[c].y;
+      for (int c = 0; c < 10; ++c) *reinterpret_cast<V*>(out + c * g.cstride) = s[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 10; ++c) {
+        if (wx) out[c * g.cstride] = s[c].x;
+        if (wy) out[c * g.cstride + 1] = s[c].y;
+      }
+    }
+    if (edge) {
+      float vx[10], vy[10];
+#pragma unroll
+      for (int c = 0; c < 10; ++c) { vx[c] = s[c].x; vy[c] = s[c].y; }
+      float* bp = reinterpret_cast<float*>(A.out) + plane_off;
+      if (wx && (y == 0 || y == g.ny - 1 || zx == 0 || zx == g.nz - 1)) write_images(g, bp, y, zx, vx, 10);
+      if (wy && (y == 0 || y == g.ny - 1 || zy == 0 || zy == g.nz - 1)) write_images(g, bp, y, zy, vy, 10);
     }
   } else {
     uint32_t code[10][2];
     float mx0 = 0.f, mx1 = 0.f;
     V nz[10];
     if (DITHER) {
-      const uint32_t gi = (uint32_t)(((int64_t)(g.gx0 + q) * g.gny + y) * g.gnz + z0);
+      const uint32_t gi = (uint32_t)(((int64_t)(g.gx0 + q) * g.gny + y) * g.gnz + zx);
       const uint32_t h0a = mix32(gi + A.step_key), h0b = mix32(gi + 1u + A.step_key);
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
@@ -253,15 +266,30 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
       code[c][0] = min(f2u16_floor(t.x), A.Q.levels[c]);
       code[c][1] = min(f2u16_floor(t.y), A.Q.levels[c]);
     }
-    uint32_t* out = reinterpret_cast<uint32_t*>(A.out) + off;
+    uint32_t wd[5][2];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      uint32_t* p = out + k * g.cstride;
-      const uint32_t w0 = __byte_perm(code[2 * k][0], code[2 * k + 1][0], 0x5410);
-      const uint32_t w1 = __byte_perm(code[2 * k][1], code[2 * k + 1][1], 0x5410);
-      if (wx && wy) *reinterpret_cast<uint2*>(p) = make_uint2(w0, w1);
-      else if (wx) p[0] = w0;
-      else if (wy) p[1] = w1;
+      wd[k][0] = __byte_perm(code[2 * k][0], code[2 * k + 1][0], 0x5410);
+      wd[k][1] = __byte_perm(code[2 * k][1], code[2 * k + 1][1], 0x5410);
+    }
+    uint32_t* out = reinterpret_cast<uint32_t*>(A.out) + off;
+    if (wx && wy) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) *reinterpret_cast<uint2*>(out + k * g.cstride) = make_uint2(wd[k][0], wd[k][1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        if (wx) out[k * g.cstride] = wd[k][0];
+        if (wy) out[k * g.cstride + 1] = wd[k][1];
+      }
+    }
+    if (edge) {
+      uint32_t vx[5], vy[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) { vx[k] = wd[k][0]; vy[k] = wd[k][1]; }
+      uint32_t* bp = reinterpret_cast<uint32_t*>(A.out) + plane_off;
+      if (wx && (y == 0 || y == g.ny - 1 || zx == 0 || zx == g.nz - 1)) write_images(g, bp, y, zx, vx, 5);
+      if (wy && (y == 0 || y == g.ny - 1 || zy == 0 || zy == g.nz - 1)) write_images(g, bp, y, zy, vy, 5);
     }
     // saturation: |r| > 1  <=>  m outside [min, max]  (rare slow path)
     const bool satx = statx && !(mx0 <= 1.0f), saty = staty && !(mx1 <= 1.0f);
@@ -301,33 +329,28 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
   item /= g.nzt;
   const int yt = item % g.nyt;
   const int xsi = item / g.nyt;
-  const int zb = zt * kZT;
-  const int zlo = zb + 1, zhi = min(zb + 1 + kZT, g.nz + 1);
-  const int y0 = yt * kRows;
-  const int yrow_u = y0 - 1 + w;
-  const int yrow = wrapi(yrow_u, g.ny);
-  const bool row_interior = (w >= 1) && (w <= kRows) && (yrow_u < g.ny);
+  const int zs0 = zt * kZT;                 // storage column of the window start
+  const int zlo = zs0, zhi = min(zs0 + kZT, g.nz);   // interior logical z range of this tile
+  const int ys0 = yt * kRows;               // storage row of warp 0
+  const int yrow = ys0 + w - 1;             // logical y of this warp's row
+  const bool row_interior = (w >= 1) && (w <= kRows) && (yrow < g.ny);
   const int xs = xsi * g.xseg, xe = min(xs + g.xseg, g.nx);
   const int NP = xe - xs + 2;
-  const bool need_p = (w < kNW - 1);   // this row feeds row+1 (cy = +1)
-  const bool need_m = (w > 0);         // feeds row-1 (cy = -1)
-  const bool need_0 = (w > 0) && (w < kNW - 1);
 
-  // this lane's cells
-  const int zu0 = zb + 2 * lane;
-  const int z0 = wrapi(zu0, g.nz);
-  const bool wx = row_interior && zu0 >= zlo && zu0 < zhi;
-  const bool wy = row_interior && zu0 + 1 >= zlo && zu0 + 1 < zhi;
+  const int zst = zs0 + 2 * lane;           // storage column of this lane's .x cell
+  const bool wx = row_interior && (zst - 1 >= zlo) && (zst - 1 < zhi);
+  const bool wy = row_interior && (zst >= zlo) && (zst < zhi);
 
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
   }
   __syncthreads();
-  if (w == 0) {
+  if (threadIdx.x == 0) {
     for (int it = 0; it < STAGES - 1 && it < NP; ++it)
-      issue_plane<NC>(A, xs - 1 + it, S.stage[it % STAGES], &S.bar[it % STAGES], zb, y0, lane);
+      issue_plane<NC>(A, xs - 1 + it, S.stage[it % STAGES], &S.bar[it % STAGES], zs0, ys0);
   }
 
   float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
@@ -338,18 +361,27 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 #pragma unroll
   for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
 
-  auto body = [&](int it, Part9& A9, Part6& B6) {
+  for (int it = 0; it < NP; ++it) {
     const int p = xs - 1 + it;
-    if (w == 0 && it + STAGES - 1 < NP) {
+    if (threadIdx.x == 0 && it + STAGES - 1 < NP) {
       const int j = it + STAGES - 1;
-      issue_plane<NC>(A, xs - 1 + j, S.stage[j % STAGES], &S.bar[j % STAGES], zb, y0, lane);
+      issue_plane<NC>(A, xs - 1 + j, S.stage[j % STAGES], &S.bar[j % STAGES], zs0, ys0);
     }
     const int q = p - 1;   // destination plane finished in this iteration
     const bool store_plane = row_interior && q >= xs && q < xe;
     uint32_t sbits = 0;
     if (SPECIAL && store_plane) {
-      const int64_t bi = ((int64_t)q * g.ny + yrow) * A.bits_row_words + (z0 >> 5);
-      sbits = __ldg(A.special_bits + bi) >> (z0 & 31);
+      const int zq = max(zst - 1, 0);   // word holding the pair (z of .x may be -1 at tile 0)
+      const int64_t bi = ((int64_t)q * g.ny + yrow) * A.bits_row_words + (zq >> 5);
+      const uint32_t wv = __ldg(A.special_bits + bi);
+      if (zst - 1 < 0) sbits = (wv & 1u) << 1;                  // only .y (z = 0) is a cell
+      else {
+        const uint32_t lo = wv >> (zq & 31);
+        // .y (z = zq + 1) may sit in the next word when zq is the last bit of a word
+        uint32_t hi = lo >> 1;
+        if ((zq & 31) == 31 && zq + 1 < g.nz) hi = __ldg(A.special_bits + bi + 1);
+        sbits = (lo & 1u) | ((hi & 1u) << 1);
+      }
     }
     const int sp = (p < 0) ? g.x_lo_src : (p >= g.nx ? g.x_hi_src : p + 1);
     const bool inflow = sp < 0;
@@ -364,27 +396,26 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
           coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
       V gz[3];
       // cx = -1 -> dest q (final contribution)
-      gz[0] = gz[1] = gz[2] = vsplat(0.f);
-      recon_cx<-1>(C, need_p, need_0, need_m, S.exch, w, lane, gz);
-      fin[0] = vadd(A9.a[0], gz[0]);
-      fin[3] = vadd(A9.a[1], gz[1]);
-      fin[9] = vadd(A9.a[2], gz[2]);
-      fin[2] = A9.a[3];
-      fin[8] = A9.a[4];
-      fin[7] = A9.a[5];
-      fin[1] = vsub(A9.b[0], gz[0]);
-      fin[6] = vsub(A9.b[1], gz[1]);
-      fin[5] = A9.b[2];
-      fin[4] = vadd(A9.b[0], gz[0]);
+      recon_cx<-1>(C, S.exch, w, lane, gz);
+      fin[0] = vadd(Ac.a[0], gz[0]);
+      fin[3] = vadd(Ac.a[1], gz[1]);
+      fin[9] = vadd(Ac.a[2], gz[2]);
+      fin[2] = Ac.a[3];
+      fin[8] = Ac.a[4];
+      fin[7] = Ac.a[5];
+      fin[1] = vsub(Ac.b[0], gz[0]);
+      fin[6] = vsub(Ac.b[1], gz[1]);
+      fin[5] = Ac.b[2];
+      fin[4] = vadd(Ac.b[0], gz[0]);
       // cx = 0 -> dest p
-      recon_cx<0>(C, need_p, need_0, need_m, S.exch, w, lane, gz);
-      nb.a[0] = vadd(B6.a[0], gz[0]);
-      nb.a[1] = vadd(B6.a[1], gz[1]);
-      nb.a[2] = vadd(B6.a[2], gz[2]);
-      nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
-      nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
+      recon_cx<0>(C, S.exch, w, lane, gz);
+      nb.a[0] = vadd(Bc.a[0], gz[0]);
+      nb.a[1] = vadd(Bc.a[1], gz[1]);
+      nb.a[2] = vadd(Bc.a[2], gz[2]);
+      nb.a[3] = Bc.a[3]; nb.a[4] = Bc.a[4]; nb.a[5] = Bc.a[5];
+      nb.b[0] = Bc.a[0]; nb.b[1] = Bc.a[1]; nb.b[2] = Bc.a[3];
       // cx = +1 -> dest p+1
-      recon_cx<1>(C, need_p, need_0, need_m, S.exch, w, lane, gz);
+      recon_cx<1>(C, S.exch, w, lane, gz);
       nn[0] = gz[0]; nn[1] = gz[1]; nn[2] = gz[2];
     }
     __syncthreads();
@@ -404,17 +435,15 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       if (store_plane) {
         const bool sx = A.do_stats && wx && !(SPECIAL && (sbits & 1u));
         const bool sy = A.do_stats && wy && !(SPECIAL && (sbits & 2u));
-        store_pair<Q16, DITHER>(A, fin, q, yrow, z0, wx, wy, sx, sy, red);
+        store_pair<Q16, DITHER>(A, fin, q, yrow, zst, wx, wy, sx, sy, red);
       }
     }
 #pragma unroll
-    for (int k = 0; k < 6; ++k) { A9.a[k] = nb.a[k]; B6.a[k] = nn[k]; }
+    for (int k = 0; k < 6; ++k) { Ac.a[k] = nb.a[k]; Bc.a[k] = nn[k]; }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) A9.b[k] = nb.b[k];
+    for (int k = 0; k < 3; ++k) Ac.b[k] = nb.b[k];
     __syncthreads();
-  };
-
-  for (int it = 0; it < NP; ++it) body(it, Ac, Bc);
+  }
 
   if (A.do_stats) {
     // block reduction of the fused statistics

@@ -2,10 +2,15 @@
 //
 // Layout: one allocation per buffer, x-plane major so that an x-plane
 // holding every component is contiguous (halo planes ship without packing):
-//     state[xs][c][y][z],   xs = 0 .. nx+1  (xs = 0 and nx+1 are ghost planes)
+//     state[xs][c][ys][zs],  xs = 0 .. nx+1 (0, nx+1: ghost planes)
+//                            ys = y + 1 in 0 .. ny+1, zs = z + 1 in 0 .. nz+1 (row stride zp)
+// The y/z ghost rows/columns hold the periodic images of the opposite edge; every kernel that
+// writes an edge cell also writes its images, so a tile never wraps and one TMA box per plane
+// covers it.
 //   fp32: c = 0..9  -> d = rho-1, j_x, j_y, j_z, sneq_xx, xy, xz, yy, yz, zz   (float)
 //   q16 : c = 0..4  -> u32 words, word k = code(2k) | code(2k+1) << 16
 #pragma once
+#include <cuda.h>
 #include <stdint.h>
 #include "hlbm_math.cuh"
 
@@ -14,13 +19,14 @@ namespace hlbm {
 constexpr int kNW = 16;          // warps per CTA = y rows held by a CTA (14 interior + 2 halo)
 constexpr int kRows = kNW - 2;   // interior rows per CTA
 constexpr int kZW = 64;          // z cells covered by one warp (32 lanes x 2 cells)
-constexpr int kZT = 60;          // interior z cells per tile (window start stays 16 B aligned)
+constexpr int kZT = 60;          // interior z cells per tile (window start 60k: 16 B-aligned TMA origin)
 constexpr int kNSlot = 18;       // exchanged values per cell pair: (cx 3) x (cy +-1) x (kz 3)
 
 struct Geo {
   int nx, ny, nz;          // local interior dims (x = slab axis)
-  int64_t cstride;         // ny*nz            elements between components
-  int64_t pstride;         // NC*ny*nz         elements between x planes
+  int zp;                  // padded row length (>= nz + 2, multiple of 4)
+  int64_t cstride;         // (ny+2)*zp        elements between components
+  int64_t pstride;         // NC*(ny+2)*zp     elements between x planes
   int x_lo_src, x_hi_src;  // storage plane read for source plane -1 / nx ; -1 => inflow constants
   int nzt, nyt, nxs, xseg; // tiling of the interior kernel
   int gx0, gny, gnz;       // slab offset in the global grid (dither key)
@@ -36,6 +42,7 @@ struct Stats {                 // device-side accumulators (reset by the host pe
 };
 
 struct StepArgs {
+  CUtensorMap tmap_in;              // 4-D map over `in`: (zs, ys, c, xs), box (64, 16, NC, 1)
   const void* in;
   void* out;
   Geo g;
@@ -48,6 +55,11 @@ struct StepArgs {
   int do_stats;
   Stats* stats;
 };
+
+// element offset of cell (y, z) of storage plane sp (component 0)
+__host__ __device__ __forceinline__ int64_t cell_off(const Geo& g, int sp, int y, int z) {
+  return (int64_t)sp * g.pstride + (int64_t)(y + 1) * g.zp + (z + 1);
+}
 
 __host__ __device__ __forceinline__ int wrapi(int a, int n) {
   a %= n;
