@@ -19,6 +19,7 @@ using namespace hlbm;
 struct hlbm_ctx {
   hlbm_config cfg{};
   int q16 = 0, NC = 10;
+  bool b16 = true;   // every component uses all 16 bits of its slot
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   size_t elem_bytes = 4;
@@ -179,6 +180,7 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
       if (c.bits[k] == 0) c.bits[k] = 16;
       if (c.bits[k] < 2 || c.bits[k] > 16) return bad("bits per component must lie in [2, 16]");
       if (!(c.qmax[k] > c.qmin[k])) return bad("quantization range needs min < max");
+      if (c.bits[k] != 16) ctx->b16 = false;
     }
   }
   if (cudaSetDevice(c.device) != cudaSuccess) return bad("cannot select CUDA device");
@@ -505,7 +507,7 @@ int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
     const int st = (with_stats && s == nsteps - 1) ? 1 : 0;
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->stream));
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->b16, ctx->stream));
     ++ctx->launches;
     if (ctx->nb) {
       CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
@@ -585,7 +587,7 @@ int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->stream));
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->b16, ctx->stream));
     ++ctx->launches;
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     if (ctx->nb) {

@@ -68,7 +68,7 @@ __device__ __forceinline__ V from_zp(V v) {   // value at (z + 1)
 template <int NC, int STAGES>
 struct Smem {
   uint32_t stage[STAGES][NC][kNW][kZW];
-  V exch[kNSlot][kNW][32];
+  V exch[2][kNSlot][kNW][32];   // double-buffered: one CTA barrier per plane
   uint64_t bar[STAGES];
   float red[kNW][5];
 };
@@ -210,7 +210,7 @@ __device__ __forceinline__ void write_images(const Geo& g, E* base_plane, int y,
 
 // store of one finished cell pair + fused statistics.  zs = storage column of the .x cell
 // (even -> 8-byte aligned pair); logical z of .x is zs - 1.
-template <bool Q16, bool DITHER>
+template <bool Q16, bool DITHER, bool B16>
 __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int zs,
                                            bool wx, bool wy, bool statx, bool staty, float red[5]) {
   const Geo& g = A.g;
@@ -242,7 +242,6 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
       if (wy && (y == 0 || y == g.ny - 1 || zy == 0 || zy == g.nz - 1)) write_images(g, bp, y, zy, vy, 10);
     }
   } else {
-    uint32_t code[10][2];
     float mx0 = 0.f, mx1 = 0.f;
     V nz[10];
     if (DITHER) {
@@ -256,21 +255,29 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
         nz[2 * k + 1] = make_float2(noise16(ha >> 16), noise16(hb >> 16));
       }
     }
+    V t[10];
 #pragma unroll
     for (int c = 0; c < 10; ++c) {
-      V t = vfma(s[c], vsplat(A.Q.enc_scale[c]), vsplat(A.Q.enc_off[c]));
-      if (DITHER) t = vadd(t, nz[c]);
+      t[c] = vfma(s[c], vsplat(A.Q.enc_scale[c]), vsplat(A.Q.enc_off[c]));
+      if (DITHER) t[c] = vadd(t[c], nz[c]);
       const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
       mx0 = fmaxf(mx0, fabsf(r.x));
       mx1 = fmaxf(mx1, fabsf(r.y));
-      code[c][0] = min(f2u16_floor(t.x), A.Q.levels[c]);
-      code[c][1] = min(f2u16_floor(t.y), A.Q.levels[c]);
     }
     uint32_t wd[5][2];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      wd[k][0] = __byte_perm(code[2 * k][0], code[2 * k + 1][0], 0x5410);
-      wd[k][1] = __byte_perm(code[2 * k][1], code[2 * k + 1][1], 0x5410);
+      if (B16) {   // 16-bit slots: the saturating cvt is the clamp
+        wd[k][0] = pack2_u16_floor(t[2 * k].x, t[2 * k + 1].x);
+        wd[k][1] = pack2_u16_floor(t[2 * k].y, t[2 * k + 1].y);
+      } else {
+        const uint32_t a0 = min(f2u16_floor(t[2 * k].x), A.Q.levels[2 * k]);
+        const uint32_t b0 = min(f2u16_floor(t[2 * k + 1].x), A.Q.levels[2 * k + 1]);
+        const uint32_t a1 = min(f2u16_floor(t[2 * k].y), A.Q.levels[2 * k]);
+        const uint32_t b1 = min(f2u16_floor(t[2 * k + 1].y), A.Q.levels[2 * k + 1]);
+        wd[k][0] = __byte_perm(a0, b0, 0x5410);
+        wd[k][1] = __byte_perm(a1, b1, 0x5410);
+      }
     }
     uint32_t* out = reinterpret_cast<uint32_t*>(A.out) + off;
     if (wx && wy) {
@@ -316,7 +323,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
   }
 }
 
-template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, int STAGES>
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool B16, int STAGES>
 __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_constant__ StepArgs A) {
   constexpr int NC = Q16 ? 5 : 10;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -349,26 +356,24 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int it = 0; it < STAGES - 1 && it < NP; ++it)
+    for (int it = 0; it < STAGES && it < NP; ++it)
       issue_plane<NC>(A, xs - 1 + it, S.stage[it % STAGES], &S.bar[it % STAGES], zs0, ys0);
   }
 
   float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-  Part9 Ac;   // dest p-1 partial
-  Part6 Bc;   // dest p partial
+  Part9 Ac, Ad;   // dest p-1 partials (two register sets: the loop is unrolled x2)
+  Part6 Bc, Bd;   // dest p partials
 #pragma unroll
   for (int k = 0; k < 6; ++k) Ac.a[k] = Bc.a[k] = vsplat(0.f);
 #pragma unroll
   for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
 
-  for (int it = 0; it < NP; ++it) {
+  // one source plane: (A9, B6) carried in, (nb, nn) carried out
+  auto body = [&](const int it, const Part9& A9, const Part6& B6, Part9& nb, Part6& nn) {
     const int p = xs - 1 + it;
-    if (threadIdx.x == 0 && it + STAGES - 1 < NP) {
-      const int j = it + STAGES - 1;
-      issue_plane<NC>(A, xs - 1 + j, S.stage[j % STAGES], &S.bar[j % STAGES], zs0, ys0);
-    }
     const int q = p - 1;   // destination plane finished in this iteration
     const bool store_plane = row_interior && q >= xs && q < xe;
+    V (*exch)[kNW][32] = S.exch[it & 1];
     uint32_t sbits = 0;
     if (SPECIAL && store_plane) {
       const int zq = max(zst - 1, 0);   // word holding the pair (z of .x may be -1 at tile 0)
@@ -377,7 +382,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       if (zst - 1 < 0) sbits = (wv & 1u) << 1;                  // only .y (z = 0) is a cell
       else {
         const uint32_t lo = wv >> (zq & 31);
-        // .y (z = zq + 1) may sit in the next word when zq is the last bit of a word
         uint32_t hi = lo >> 1;
         if ((zq & 31) == 31 && zq + 1 < g.nz) hi = __ldg(A.special_bits + bi + 1);
         sbits = (lo & 1u) | ((hi & 1u) << 1);
@@ -387,8 +391,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     const bool inflow = sp < 0;
     mbar_wait(&S.bar[it % STAGES], (uint32_t)((it / STAGES) & 1));
     V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
-    Part9 nb;    // dest p after this source
-    V nn[6];     // dest p+1 after this source
     {
       V s[10];
       load_state<Q16>(S.stage[it % STAGES], w, lane, inflow, A, s);
@@ -396,53 +398,57 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
           coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
       V gz[3];
       // cx = -1 -> dest q (final contribution)
-      recon_cx<-1>(C, S.exch, w, lane, gz);
-      fin[0] = vadd(Ac.a[0], gz[0]);
-      fin[3] = vadd(Ac.a[1], gz[1]);
-      fin[9] = vadd(Ac.a[2], gz[2]);
-      fin[2] = Ac.a[3];
-      fin[8] = Ac.a[4];
-      fin[7] = Ac.a[5];
-      fin[1] = vsub(Ac.b[0], gz[0]);
-      fin[6] = vsub(Ac.b[1], gz[1]);
-      fin[5] = Ac.b[2];
-      fin[4] = vadd(Ac.b[0], gz[0]);
+      recon_cx<-1>(C, exch, w, lane, gz);
+      fin[0] = vadd(A9.a[0], gz[0]);
+      fin[3] = vadd(A9.a[1], gz[1]);
+      fin[9] = vadd(A9.a[2], gz[2]);
+      fin[2] = A9.a[3];
+      fin[8] = A9.a[4];
+      fin[7] = A9.a[5];
+      fin[1] = vsub(A9.b[0], gz[0]);
+      fin[6] = vsub(A9.b[1], gz[1]);
+      fin[5] = A9.b[2];
+      fin[4] = vadd(A9.b[0], gz[0]);
       // cx = 0 -> dest p
-      recon_cx<0>(C, S.exch, w, lane, gz);
-      nb.a[0] = vadd(Bc.a[0], gz[0]);
-      nb.a[1] = vadd(Bc.a[1], gz[1]);
-      nb.a[2] = vadd(Bc.a[2], gz[2]);
-      nb.a[3] = Bc.a[3]; nb.a[4] = Bc.a[4]; nb.a[5] = Bc.a[5];
-      nb.b[0] = Bc.a[0]; nb.b[1] = Bc.a[1]; nb.b[2] = Bc.a[3];
+      recon_cx<0>(C, exch, w, lane, gz);
+      nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
+      nb.a[0] = vadd(B6.a[0], gz[0]);
+      nb.a[1] = vadd(B6.a[1], gz[1]);
+      nb.a[2] = vadd(B6.a[2], gz[2]);
+      nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
       // cx = +1 -> dest p+1
-      recon_cx<1>(C, S.exch, w, lane, gz);
-      nn[0] = gz[0]; nn[1] = gz[1]; nn[2] = gz[2];
+      recon_cx<1>(C, exch, w, lane, gz);
+      nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
     }
-    __syncthreads();
+    __syncthreads();   // exch[it&1] complete; every thread is done reading stage it%STAGES
+    if (threadIdx.x == 0 && it + STAGES < NP) {
+      const int j = it + STAGES;
+      issue_plane<NC>(A, xs - 1 + j, S.stage[j % STAGES], &S.bar[j % STAGES], zs0, ys0);
+    }
     if (row_interior) {
       V t[3], d[2];
-      ystage<-1>(S.exch, w, lane, t, d);
+      ystage<-1>(exch, w, lane, t, d);
       fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
       fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
       fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
       fin[4] = vadd(fin[4], t[0]);
-      ystage<0>(S.exch, w, lane, t, d);
+      ystage<0>(exch, w, lane, t, d);
       nb.a[0] = vadd(nb.a[0], t[0]); nb.a[1] = vadd(nb.a[1], t[1]); nb.a[2] = vadd(nb.a[2], t[2]);
       nb.a[3] = vadd(nb.a[3], d[0]); nb.a[4] = vadd(nb.a[4], d[1]); nb.a[5] = vadd(nb.a[5], t[0]);
-      ystage<1>(S.exch, w, lane, t, d);
-      nn[0] = vadd(nn[0], t[0]); nn[1] = vadd(nn[1], t[1]); nn[2] = vadd(nn[2], t[2]);
-      nn[3] = d[0]; nn[4] = d[1]; nn[5] = t[0];
+      ystage<1>(exch, w, lane, t, d);
+      nn.a[0] = vadd(nn.a[0], t[0]); nn.a[1] = vadd(nn.a[1], t[1]); nn.a[2] = vadd(nn.a[2], t[2]);
+      nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
       if (store_plane) {
         const bool sx = A.do_stats && wx && !(SPECIAL && (sbits & 1u));
         const bool sy = A.do_stats && wy && !(SPECIAL && (sbits & 2u));
-        store_pair<Q16, DITHER>(A, fin, q, yrow, zst, wx, wy, sx, sy, red);
+        store_pair<Q16, DITHER, B16>(A, fin, q, yrow, zst, wx, wy, sx, sy, red);
       }
     }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) { Ac.a[k] = nb.a[k]; Bc.a[k] = nn[k]; }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) Ac.b[k] = nb.b[k];
-    __syncthreads();
+  };
+
+  for (int it = 0; it < NP; it += 2) {
+    body(it, Ac, Bc, Ad, Bd);
+    if (it + 1 < NP) body(it + 1, Ad, Bd, Ac, Bc);
   }
 
   if (A.do_stats) {
@@ -484,12 +490,12 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 }
 
 // ------------------------------------------------------------------------ host launcher
-template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER>
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool B16>
 static cudaError_t launch_t(const StepArgs& A, int nblocks, cudaStream_t st) {
-  constexpr int STAGES = Q16 ? 4 : 3;
+  constexpr int STAGES = Q16 ? 3 : 2;
   constexpr int NC = Q16 ? 5 : 10;
   const size_t smem = sizeof(Smem<NC, STAGES>);
-  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STAGES>;
+  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, B16, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<nblocks, kNW * 32, smem, st>>>(A);
@@ -497,25 +503,25 @@ static cudaError_t launch_t(const StepArgs& A, int nblocks, cudaStream_t st) {
 }
 
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
-                                  cudaStream_t st) {
+                                  bool b16, cudaStream_t st) {
   const int nblocks = A.g.nzt * A.g.nyt * A.g.nxs;
   if (nblocks == 0) return cudaSuccess;
-#define HLBM_DISPATCH(Q, F, S, D)                                              \
-  if (q16 == Q && force == F && special == S && dither == D)                   \
-    return launch_t<Q, F, S, D>(A, nblocks, st);
-  HLBM_DISPATCH(false, false, false, false)
-  HLBM_DISPATCH(false, false, true, false)
-  HLBM_DISPATCH(false, true, false, false)
-  HLBM_DISPATCH(false, true, true, false)
-  HLBM_DISPATCH(true, false, false, false)
-  HLBM_DISPATCH(true, false, true, false)
-  HLBM_DISPATCH(true, true, false, false)
-  HLBM_DISPATCH(true, true, true, false)
-  HLBM_DISPATCH(true, false, false, true)
-  HLBM_DISPATCH(true, false, true, true)
-  HLBM_DISPATCH(true, true, false, true)
-  HLBM_DISPATCH(true, true, true, true)
-#undef HLBM_DISPATCH
+#define HLBM_F(F, S)                                                               \
+  if (!q16 && force == F && special == S) return launch_t<false, F, S, false, false>(A, nblocks, st);
+  HLBM_F(false, false) HLBM_F(false, true) HLBM_F(true, false) HLBM_F(true, true)
+#undef HLBM_F
+#define HLBM_Q(F, S, D, B)                                                                     \
+  if (q16 && force == F && special == S && dither == D && b16 == B)                           \
+    return launch_t<true, F, S, D, B>(A, nblocks, st);
+  HLBM_Q(false, false, false, true) HLBM_Q(false, true, false, true)
+  HLBM_Q(true, false, false, true) HLBM_Q(true, true, false, true)
+  HLBM_Q(false, false, true, true) HLBM_Q(false, true, true, true)
+  HLBM_Q(true, false, true, true) HLBM_Q(true, true, true, true)
+  HLBM_Q(false, false, false, false) HLBM_Q(false, true, false, false)
+  HLBM_Q(true, false, false, false) HLBM_Q(true, true, false, false)
+  HLBM_Q(false, false, true, false) HLBM_Q(false, true, true, false)
+  HLBM_Q(true, false, true, false) HLBM_Q(true, true, true, false)
+#undef HLBM_Q
   return cudaErrorInvalidValue;
 }
 

@@ -14,7 +14,7 @@ struct MaskGeo {
 };
 
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
-                                  cudaStream_t st);
+                                  bool b16, cudaStream_t st);
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,

@@ -237,4 +237,13 @@ __device__ __forceinline__ uint32_t f2u16_floor(float t) {
   return r;
 }
 
+// two 16-bit codes floor(lo), floor(hi), saturated to [0, 65535], packed lo | hi << 16
+__device__ __forceinline__ uint32_t pack2_u16_floor(float lo, float hi) {
+  uint32_t r;
+  asm("{\n .reg .u16 a, b;\n cvt.rmi.u16.f32 a, %1;\n cvt.rmi.u16.f32 b, %2;\n mov.b32 %0, {a, b};\n}"
+      : "=r"(r)
+      : "f"(lo), "f"(hi));
+  return r;
+}
+
 }  // namespace hlbm
