@@ -71,6 +71,8 @@ typedef struct hlbm_stats {
 } hlbm_stats;
 
 const char* hlbm_version(void);
+/* number of visible CUDA devices (0 when no driver / GPU) */
+int hlbm_device_count(void);
 
 /* SimGrid + SolverConfig construction.  Validates tau > 1/2
  * (collision.py:102-103, 203-204) and the grid (nz % 4 == 0). */

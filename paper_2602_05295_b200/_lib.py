@@ -46,6 +46,7 @@ _P = C.c_void_p
 _DP = C.POINTER(C.c_double)
 SIGNATURES = {
     "hlbm_version": (C.c_char_p, []),
+    "hlbm_device_count": (C.c_int, []),
     "hlbm_create": (C.c_int, [C.POINTER(HlbmConfig), C.POINTER(_P)]),
     "hlbm_destroy": (None, [_P]),
     "hlbm_last_error": (C.c_char_p, [_P]),

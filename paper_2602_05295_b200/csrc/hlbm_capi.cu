@@ -141,6 +141,15 @@ extern "C" {
 
 const char* hlbm_version(void) { return "hlbm-b200 0.1 (sm_100a)"; }
 
+int hlbm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 const char* hlbm_last_error(const hlbm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {

@@ -1,0 +1,105 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE package.
+
+Run here (not on the GPU box, where /root/reference does not exist):
+    python tests/golden/gen_golden.py
+It imports momentlbm from /root/reference/pkg/src (or baseline/_ref) and records
+outputs of the reference's own functions:
+  lattice.npz        make_lattice("D3Q27") tables (lattice.py:172-211)
+  moments.npz        reconstruct_distributions / moments_from_distributions /
+                     neq_decompose on random moment sets (moments.py:25-102)
+  collision.npz      collide_moments with and without a body force (collision.py:137-194)
+  step16.npz         one periodic step of a random 16^3 state composed from the reference
+                     functions + np.roll pull streaming (SURVEY.md §8c golden vector 1)
+  tgv32.npz          Taylor-Green 32^3 after 10 steps, same composition
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+for cand in ("/root/reference/pkg/src", str(ROOT / "baseline" / "_ref")):
+    if Path(cand, "momentlbm").exists():
+        sys.path.insert(0, cand)
+        break
+
+import momentlbm.collision as RC  # noqa: E402
+import momentlbm.lattice as RL  # noqa: E402
+import momentlbm.moments as RM  # noqa: E402
+
+LAT = RL.make_lattice("D3Q27")
+
+
+def ref_step(rho, mom, stress, tau, force=None):
+    """Alg. 2 from the reference's own functions."""
+    r, m, s = RC.collide_moments(rho, mom, stress, force, tau, 3)
+    f = RM.reconstruct_distributions(r, m, s, LAT)
+    fs = np.stack([np.roll(f[i], shift=tuple(LAT.velocities[i]), axis=(0, 1, 2)) for i in range(27)])
+    return RM.moments_from_distributions(fs, LAT)
+
+
+def random_state(shape, seed, drho, umax, sneq):
+    rng = np.random.default_rng(seed)
+    rho = 1.0 + rng.uniform(-drho, drho, shape)
+    mom = rho * rng.uniform(-umax, umax, (3,) + tuple(shape))
+    n = rng.uniform(-sneq, sneq, (6,) + tuple(shape))
+    return rho, mom, RM.neq_recompose(rho, mom, n)
+
+
+def taylor_green(n, u0=0.05):
+    k = 2 * np.pi / n
+    x = np.arange(n)[:, None, None]
+    y = np.arange(n)[None, :, None]
+    z = np.arange(n)[None, None, :]
+    ux = u0 * np.sin(k * x) * np.cos(k * y) * np.cos(k * z)
+    uy = -u0 * np.cos(k * x) * np.sin(k * y) * np.cos(k * z)
+    uz = np.zeros_like(ux + uy)
+    rho = 1.0 + 3.0 * (u0 ** 2 / 16.0) * (np.cos(2 * k * x) + np.cos(2 * k * y)) * (np.cos(2 * k * z) + 2.0)
+    rho = np.broadcast_to(rho, (n, n, n)).astype(np.float64)
+    mom = np.stack([rho * ux, rho * uy, rho * uz])
+    return rho, mom, RM.neq_recompose(rho, mom, np.zeros((6, n, n, n)))
+
+
+def main():
+    h = LAT.hermite
+    np.savez_compressed(HERE / "lattice.npz", velocities=LAT.velocities, weights=LAT.weights,
+                        opposite=LAT.opposite, h2=h.h2, h2c=h.h2_contract, h3=h.h3)
+
+    rho, mom, st = random_state((64,), 0, 0.3, 0.4, 0.1)
+    f = RM.reconstruct_distributions(rho, mom, st, LAT)
+    rng = np.random.default_rng(1)
+    fr = LAT.weights[:, None] * (1.0 + rng.uniform(-0.2, 0.2, (27, 64)))
+    r2, m2, s2 = RM.moments_from_distributions(fr, LAT)
+    np.savez_compressed(HERE / "moments.npz", rho=rho, mom=mom, stress=st, f=f, f_rand=fr,
+                        rho_of_f=r2, mom_of_f=m2, stress_of_f=s2,
+                        sneq=RM.neq_decompose(rho, mom, st))
+
+    F = np.array([1e-4, -2e-4, 3e-5])
+    c0 = RC.collide_moments(rho, mom, st, None, 0.53, 3)
+    c1 = RC.collide_moments(rho, mom, st, F, 0.8, 3)
+    np.savez_compressed(HERE / "collision.npz", rho=rho, mom=mom, stress=st, force=F,
+                        tau0=0.53, rho0=c0[0], mom0=c0[1], stress0=c0[2],
+                        tau1=0.8, rho1=c1[0], mom1=c1[1], stress1=c1[2])
+
+    tau = 0.5 + 3 * 0.02
+    rho, mom, st = random_state((16, 16, 16), 0, 0.1, 0.1, 0.01)
+    out = ref_step(rho, mom, st, tau)
+    np.savez_compressed(HERE / "step16.npz", tau=tau, rho=rho, mom=mom, stress=st,
+                        rho1=out[0], mom1=out[1], stress1=out[2])
+
+    tau = 0.5 + 3 * 0.01
+    r, m, s = taylor_green(32)
+    init = (r, m, s)
+    for _ in range(10):
+        r, m, s = ref_step(r, m, s, tau)
+    np.savez_compressed(HERE / "tgv32.npz", tau=tau, steps=10, rho0=init[0], mom0=init[1],
+                        stress0=init[2], rho=r, mom=m, stress=s)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,93 @@
+"""x-slab decomposition + halo exchange (paper_2602_05295_b200.distributed) on CPU with gloo,
+world size 2 and 3, using the oracle as each rank's slab stepper: the gathered result must
+equal the single-domain oracle step."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import step as OS
+from paper_2602_05295_b200.distributed import exchange_halos, partition
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, bc_x, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gdims = (13, 6, 8)
+        bc = OS.BC(x=bc_x, u_in=(0.04, 0.0, 0.0))
+        r, m, s = OS.random_state(gdims, seed=9, drho=0.05, umax=0.05, sneq=0.005)
+        plan = partition(gdims[0], world, bc_x == ("periodic", "periodic"))[rank]
+        sl = slice(plan.x0, plan.x0 + plan.nx)
+        st = np.concatenate([r[None, sl], m[:, sl], s[:, sl]]).copy()       # (10, nx, ny, nz)
+        for _ in range(steps):
+            send_lo = torch.from_numpy(st[:, 0].copy())
+            send_hi = torch.from_numpy(st[:, -1].copy())
+            recv_lo = torch.zeros_like(send_lo)
+            recv_hi = torch.zeros_like(send_hi)
+            exchange_halos(send_lo, send_hi, recv_lo, recv_hi, plan)
+            # x ghosts: neighbour planes, or the BC at a domain face (oracle/step.py:_pad_axis)
+            full = OS.pad_state(st[0], st[1:4], st[4:10], bc)                  # BC-padded
+            if plan.lo is not None:
+                full[:, 0] = _pad_yz(recv_lo.numpy(), bc)
+            if plan.hi is not None:
+                full[:, -1] = _pad_yz(recv_hi.numpy(), bc)
+            rr, mm, ss = OS.step_padded(full, 0.56)
+            st = np.concatenate([rr[None], mm, ss])
+        out[rank] = (plan.x0, st)
+    finally:
+        dist.destroy_process_group()
+
+
+def _pad_yz(plane, bc):
+    p = OS._pad_axis(plane, 1, bc.y)
+    return OS._pad_axis(p, 2, bc.z)
+
+
+def _run(world, bc_x, steps):
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, bc_x, steps, out), nprocs=world, join=True)
+    gdims = (13, 6, 8)
+    bc = OS.BC(x=bc_x, u_in=(0.04, 0.0, 0.0))
+    r, m, s = OS.random_state(gdims, seed=9, drho=0.05, umax=0.05, sneq=0.005)
+    for _ in range(steps):
+        r, m, s = OS.fluid_step(r, m, s, 0.56, bc)
+    ref = np.concatenate([r[None], m, s])
+    got = np.zeros_like(ref)
+    for rank in range(world):
+        x0, st = out[rank]
+        got[:, x0:x0 + st.shape[1]] = st
+    return got, ref
+
+
+@pytest.mark.parametrize("world,bc_x", [(2, ("periodic", "periodic")), (3, ("periodic", "periodic")),
+                                        (2, ("inflow", "outflow"))])
+def test_slab_exchange_reproduces_single_domain(world, bc_x):
+    got, ref = _run(world, bc_x, 3)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14)
+
+
+def test_partition_covers_domain():
+    for gnx, world in ((2048, 8), (13, 3), (7, 7)):
+        plans = partition(gnx, world, True)
+        assert sum(p.nx for p in plans) == gnx
+        assert plans[0].x0 == 0 and all(plans[i].x0 + plans[i].nx == plans[i + 1].x0 for i in range(world - 1))
+        assert all(p.lo == (p.rank - 1) % world and p.hi == (p.rank + 1) % world for p in plans) or world == 1
+    plans = partition(16, 4, False)
+    assert plans[0].lo is None and plans[-1].hi is None

@@ -1,0 +1,227 @@
+"""Parity of the CUDA path (libhlbm.so on cuda:0) with the reference and the oracle.
+
+Tolerances (stated per the north star):
+  * fp32: per-moment relative L2 error ||m_gpu - m_ref|| / ||m_ref|| <= 1e-5 for each of the
+    reference's moments rho, rho u, rho S (MomentSet fields, moments.py:136-172).
+  * q16: code difference against the oracle's own quantized path (decode -> float64 step ->
+    encode, oracle/step.py:fluid_step_q16) <= 1 LSB after one step; <= 8 LSB after 50 steps.
+  * boundary lists / link masks: bit-exact.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import codec
+from oracle import step as OS
+from oracle.moments import neq_decompose, neq_recompose
+from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
+from paper_2602_05295_b200.geometry import sphere_mask
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+FP32_TOL = 1e-5
+
+
+def moment_errors(got, ref, sel=None):
+    out = []
+    for g, r in zip(got, ref):
+        if sel is not None:
+            g, r = g[..., sel], r[..., sel]
+        out.append(float(np.linalg.norm(g - r) / np.linalg.norm(r)))
+    return out   # [rho, mom, stress]
+
+
+def run_gpu(state, cfg, steps, mask=None, reference_kernel=False):
+    shape = state[0].shape
+    with Solver(SimGrid(shape, mask), cfg) as s:
+        s.set_moments(*state)
+        if reference_kernel:
+            s.step_reference(steps)
+        else:
+            s.step(steps)
+        return s.moments()
+
+
+def test_golden_step16_matches_reference():
+    z = np.load(G / "step16.npz")
+    cfg = SolverConfig(nu=(float(z["tau"]) - 0.5) / 3)
+    got = run_gpu((z["rho"], z["mom"], z["stress"]), cfg, 1)
+    err = moment_errors(got, (z["rho1"], z["mom1"], z["stress1"]))
+    assert max(err) <= FP32_TOL, err
+
+
+def test_golden_tgv32_matches_reference():
+    z = np.load(G / "tgv32.npz")
+    cfg = SolverConfig(nu=(float(z["tau"]) - 0.5) / 3)
+    got = run_gpu((z["rho0"], z["mom0"], z["stress0"]), cfg, int(z["steps"]))
+    err = moment_errors(got, (z["rho"], z["mom"], z["stress"]))
+    assert max(err) <= FP32_TOL, err
+
+
+def test_tgv64_200_steps_config1():
+    """BASELINE config 1: TGV 64^3, fp32, periodic, 200 steps vs the oracle."""
+    state = OS.taylor_green(64)
+    cfg = SolverConfig(nu=0.01)
+    got = run_gpu(state, cfg, 200)
+    ref = OS.run(*state, cfg.tau, 200)
+    err = moment_errors(got, ref)
+    print("TGV64x200 per-moment rel errors (rho, mom, stress):", err)
+    assert max(err) <= FP32_TOL, err
+
+
+@pytest.mark.parametrize("shape,steps", [((16, 16, 16), 1), ((20, 30, 68), 3), ((7, 40, 132), 2)])
+@pytest.mark.parametrize("kernel", ["interior", "pull"])
+def test_random_states(shape, steps, kernel):
+    state = OS.random_state(shape, seed=1, drho=0.05, umax=0.08, sneq=0.005)
+    cfg = SolverConfig(nu=0.02)
+    got = run_gpu(state, cfg, steps, reference_kernel=(kernel == "pull"))
+    ref = OS.run(*state, cfg.tau, steps)
+    err = moment_errors(got, ref)
+    assert max(err) <= FP32_TOL, err
+
+
+def test_body_force():
+    state = OS.random_state((12, 16, 24), seed=2, drho=0.05, umax=0.05, sneq=0.005)
+    F = (2e-5, -1e-5, 3e-5)
+    cfg = SolverConfig(nu=0.02, force=F)
+    got = run_gpu(state, cfg, 3)
+    ref = OS.run(*state, cfg.tau, 3, force=np.array(F))
+    err = moment_errors(got, ref)
+    assert max(err) <= FP32_TOL, err
+
+
+def _channel_state(shape, mask, u0):
+    rho = np.ones(shape)
+    u = np.zeros((3,) + shape)
+    u[0] = u0
+    u[:, mask.astype(bool)] = 0
+    mom = rho * u
+    return rho, mom, neq_recompose(rho, mom, np.zeros((6,) + shape))
+
+
+@pytest.mark.parametrize("bcname", ["channel", "closed", "walls_yz"])
+def test_solids_and_domain_bcs(bcname):
+    shape = (40, 24, 28)
+    mask = sphere_mask(shape, (14, 11.5, 13.5), 5)
+    if bcname == "channel":
+        bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("wall", "wall")}
+    elif bcname == "closed":
+        bc = {"x": ("wall", "wall"), "y": ("wall", "wall"), "z": ("wall", "wall")}
+    else:
+        bc = {"x": ("periodic", "periodic"), "y": ("wall", "wall"), "z": ("wall", "wall")}
+    cfg = SolverConfig(nu=0.02, bc=bc, u_in=(0.05, 0, 0))
+    obc = OS.BC(x=bc["x"], y=bc["y"], z=bc["z"], u_in=(0.05, 0, 0))
+    cells, masks = OS.boundary_lists(mask, obc)
+    state = _channel_state(shape, mask, 0.05 if bcname == "channel" else 0.02)
+    with Solver(SimGrid(shape, mask), cfg) as s:
+        gc, gm = s.boundary()
+        assert np.array_equal(gc, cells)          # bit-exact lists and link masks
+        assert np.array_equal(gm, masks)
+        s.set_moments(*state)
+        st = s.step(5)
+        got = s.moments()
+    ref = state
+    for _ in range(5):
+        ref = OS.fluid_step(*ref, cfg.tau, obc, None, mask)
+    fl = ~mask.astype(bool)
+    err = moment_errors(got, ref, fl)
+    assert max(err) <= FP32_TOL, err
+    assert st.mass == pytest.approx(ref[0][fl].sum(), rel=1e-7)
+    np.testing.assert_allclose(st.momentum, ref[1][:, fl].sum(axis=1), atol=1e-6 * fl.sum())
+    # solid cells hold the rest state
+    assert np.all(got[0][~fl] == 1.0) and np.all(got[1][:, ~fl] == 0.0)
+
+
+def test_stats_match_oracle_sums():
+    state = OS.random_state((16, 20, 24), seed=5, drho=0.05, umax=0.08, sneq=0.005)
+    cfg = SolverConfig(nu=0.02)
+    with Solver(SimGrid((16, 20, 24)), cfg) as s:
+        s.set_moments(*state)
+        st = s.step(2)
+    ref = OS.run(*state, cfg.tau, 2)
+    assert st.mass == pytest.approx(ref[0].sum(), rel=1e-7)
+    np.testing.assert_allclose(st.momentum, ref[1].sum(axis=(1, 2, 3)), atol=1e-4)
+    assert st.max_u == pytest.approx(np.sqrt(((ref[1] / ref[0]) ** 2).sum(0)).max(), rel=1e-5)
+    assert st.n_fluid == 16 * 20 * 24
+
+
+def test_divergence_raises_floating_point_error():
+    shape = (8, 8, 8)
+    rho = np.ones(shape)
+    mom = np.zeros((3,) + shape)
+    mom[0] = 0.95
+    st = neq_recompose(rho, mom, np.zeros((6,) + shape))
+    with Solver(SimGrid(shape), SolverConfig(nu=0.02)) as s:
+        s.set_moments(rho, mom, st)
+        with pytest.raises(FloatingPointError):
+            s.step(1)
+
+
+def test_moment_set_accessor():
+    state = OS.random_state((8, 8, 8), seed=6, drho=0.05, umax=0.05, sneq=0.005)
+    with Solver(SimGrid((8, 8, 8)), SolverConfig(nu=0.02)) as s:
+        s.set_moments(*state)
+        ms = s.moment_set(3, 4, 5)
+        np.testing.assert_allclose(ms.rho, state[0][3, 4, 5], rtol=1e-6)
+        np.testing.assert_allclose(ms.velocity, state[1][:, 3, 4, 5] / state[0][3, 4, 5], atol=1e-7)
+        with pytest.raises(ValueError):
+            s.set_moments(-state[0], state[1], state[2])      # rho <= 0 (moments.py:147)
+
+
+# ------------------------------------------------------------------ 16-bit path
+
+def _q16_case(shape, seed, quant, steps, dither=False, tau=0.56):
+    state = OS.random_state(shape, seed=seed, drho=0.05, umax=0.05, sneq=0.005)
+    w0, _ = codec.encode_state(state[0], state[1], neq_decompose(*state),
+                               np.array(quant.mmin), np.array(quant.mmax), np.array(quant.bits))
+    cfg = SolverConfig(nu=(tau - 0.5) / 3, precision="q16", quant=quant, seed=7)
+    with Solver(SimGrid(shape), cfg) as s:
+        s.codes = w0
+        for _ in range(steps):
+            s.step(1)
+        got = s.codes
+    ref = w0
+    for k in range(steps):
+        ref, _ = OS.fluid_step_q16(ref, cfg.tau, k, mmin=np.array(quant.mmin), mmax=np.array(quant.mmax),
+                                   bits=np.array(quant.bits), dither=dither, seed=7)
+    return np.abs(codec.unpack(got).astype(np.int64) - codec.unpack(ref).astype(np.int64))
+
+
+@pytest.mark.parametrize("dither", [False, True])
+def test_q16_one_step_within_1_lsb(dither):
+    d = _q16_case((16, 24, 32), 2, QuantSpec(dither=dither), 1, dither)
+    assert d.max() <= 1
+    assert np.mean(d > 0) < 0.01
+
+
+@pytest.mark.parametrize("preset", ["16/15", "14/13", "12/11"])
+def test_q16_bit_presets_one_step(preset):
+    d = _q16_case((12, 16, 32), 3, QuantSpec.preset(preset), 1)
+    assert d.max() <= 1
+
+
+def test_q16_fifty_steps_within_8_lsb():
+    d = _q16_case((12, 20, 64), 4, QuantSpec(), 50)
+    print("q16 50 steps: max LSB", d.max(), "mean", d.mean())
+    assert d.max() <= 8
+
+
+def test_q16_saturation_counts():
+    shape = (12, 16, 32)
+    q = QuantSpec(mmin=(0.995,) + QuantSpec().mmin[1:], mmax=(1.005,) + QuantSpec().mmax[1:])
+    state = OS.random_state(shape, seed=8, drho=0.004, umax=0.05, sneq=0.002)
+    w0, _ = codec.encode_state(state[0], state[1], neq_decompose(*state), np.array(q.mmin), np.array(q.mmax))
+    cfg = SolverConfig(nu=0.02, precision="q16", quant=q)
+    with Solver(SimGrid(shape), cfg) as s:
+        s.codes = w0
+        st = s.step(1)
+    rho, mom, sneq = codec.decode_state(w0, np.array(q.mmin), np.array(q.mmax))
+    r, m, sn = OS.fluid_step(rho, mom, neq_recompose(rho, mom, sneq), cfg.tau)
+    lo, hi = q.mmin[0], q.mmax[0]
+    clear = np.count_nonzero((r < lo - 1e-6) | (r > hi + 1e-6))
+    loose = np.count_nonzero((r < lo + 1e-6) | (r > hi - 1e-6))
+    assert clear > 0
+    assert clear <= st.saturation[0] <= loose
+    assert np.all(st.saturation[1:] == 0)

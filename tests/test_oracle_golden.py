@@ -1,0 +1,75 @@
+"""The CPU oracle (oracle/) pinned against outputs of the reference package itself.
+
+Fixtures in tests/golden/ were produced by tests/golden/gen_golden.py, which runs
+/root/reference/pkg/src/momentlbm (lattice.py, moments.py, collision.py)."""
+
+from pathlib import Path
+
+import numpy as np
+
+from oracle import collision as OC
+from oracle import lattice as OL
+from oracle import moments as OM
+from oracle import step as OS
+
+G = Path(__file__).resolve().parent / "golden"
+
+
+def load(name):
+    return np.load(G / name)
+
+
+def test_lattice_tables_exact():
+    z = load("lattice.npz")
+    assert np.array_equal(z["velocities"], OL.C)
+    assert np.array_equal(z["weights"], OL.W)
+    assert np.array_equal(z["opposite"], OL.OPP)
+    assert np.array_equal(z["h2"], OL.H2)
+    assert np.array_equal(z["h2c"], OL.H2C)
+    assert np.array_equal(z["h3"], OL.H3)
+
+
+def test_lattice_isotropy_exact():
+    # SPEC.md:567 acceptance 1 (rational check), lattice.py:127-139
+    assert OL.check_isotropy()
+    assert OL.W_EXACT[0] == OL.Fraction(8, 27) if hasattr(OL, "Fraction") else True
+
+
+def test_moments_against_reference():
+    z = load("moments.npz")
+    f = OM.reconstruct_distributions(z["rho"], z["mom"], z["stress"])
+    assert np.array_equal(f, z["f"])
+    r, m, s = OM.moments_from_distributions(z["f_rand"])
+    assert np.array_equal(r, z["rho_of_f"])
+    assert np.array_equal(m, z["mom_of_f"])
+    assert np.array_equal(s, z["stress_of_f"])
+    assert np.array_equal(OM.neq_decompose(z["rho"], z["mom"], z["stress"]), z["sneq"])
+
+
+def test_collision_against_reference():
+    z = load("collision.npz")
+    for k, force in ((0, None), (1, z["force"])):
+        r, m, s = OC.collide_moments(z["rho"], z["mom"], z["stress"], force, float(z[f"tau{k}"]))
+        assert np.array_equal(r, z[f"rho{k}"])
+        assert np.array_equal(m, z[f"mom{k}"])
+        assert np.array_equal(s, z[f"stress{k}"])
+
+
+def test_periodic_step_against_reference_composition():
+    z = load("step16.npz")
+    r, m, s = OS.fluid_step(z["rho"], z["mom"], z["stress"], float(z["tau"]))
+    np.testing.assert_allclose(r, z["rho1"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(m, z["mom1"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(s, z["stress1"], rtol=0, atol=1e-15)
+
+
+def test_tgv32_ten_steps_against_reference_composition():
+    z = load("tgv32.npz")
+    r, m, s = OS.run(z["rho0"], z["mom0"], z["stress0"], float(z["tau"]), int(z["steps"]))
+    np.testing.assert_allclose(r, z["rho"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(m, z["mom"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(s, z["stress"], rtol=0, atol=1e-14)
+    # and the oracle's own TGV initialisation is the fixture's
+    r0, m0, s0 = OS.taylor_green(32)
+    np.testing.assert_allclose(r0, z["rho0"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(m0, z["mom0"], rtol=0, atol=1e-15)
