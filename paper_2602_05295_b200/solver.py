@@ -326,13 +326,19 @@ class Solver:
     def link_masks(self):
         return self.boundary()[1]
 
+    def get_codes(self, out=None):
+        """Raw packed q16 words (5, nx, ny, nz) uint32, optionally into a caller buffer."""
+        nx, ny, nz = self.grid.dims
+        w = np.empty((5, nx, ny, nz), dtype=np.uint32) if out is None else out
+        if w.shape != (5, nx, ny, nz) or w.dtype != np.uint32 or not w.flags.c_contiguous:
+            raise ValueError("codes buffer must be a contiguous (5, nx, ny, nz) uint32 array")
+        self._chk(self._lib.hlbm_get_codes(self._ctx, _lib.u32ptr(w)))
+        return w
+
     @property
     def codes(self):
         """Raw packed q16 words (5, nx, ny, nz) uint32."""
-        nx, ny, nz = self.grid.dims
-        w = np.empty((5, nx, ny, nz), dtype=np.uint32)
-        self._chk(self._lib.hlbm_get_codes(self._ctx, _lib.u32ptr(w)))
-        return w
+        return self.get_codes()
 
     @codes.setter
     def codes(self, words):
