@@ -33,6 +33,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -68,8 +71,11 @@ __device__ __forceinline__ V from_zp(V v) {   // value at (z + 1)
 template <int NC, int STAGES>
 struct Smem {
   uint32_t stage[STAGES][NC][kNW][kZW];
-  V exch[2][kNSlot][kNW][32];   // double-buffered: one CTA barrier per plane
-  uint64_t bar[STAGES];
+  V exch[2][kNSlot][kNW][32];   // double-buffered y exchange
+  uint64_t bar[STAGES];         // TMA stage full (1 arrival + tx bytes)
+  uint64_t full[2][kNW];        // warp w's exchange slots of buffer b written (1 arrival)
+  uint64_t empty[2][kNW];       // ... consumed by every y-stage neighbour of w
+  uint32_t stage_cnt[STAGES];   // warps done reading a stage; the last one refills it
   float red[kNW][5];
 };
 
@@ -104,15 +110,19 @@ struct Part6 {   // only the cx=+1 contribution of source q-1: kx=1/kx=2 partial
 // reconstruction of the 9 populations with a given cx, z-stage, hand-off of the cy = +-1
 // results to shared memory; returns the cy = 0 results g[kz] (added to the x accumulators
 // before the barrier so nothing but the accumulators is live across it).
+//
+// Centre weights omega(0) = 4 are not multiplied in: the cx = 0 branch runs at 1/4 scale and
+// the cy = 0 results at 1/4 scale; the consumers fold the factor into their FMAs.  Scaling by
+// a power of two commutes with rounding, so the results are bit-identical to the unscaled
+// evaluation.
 template <int CX>
 __device__ __forceinline__ void recon_cx(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane,
                                          V g0out[3]) {
   V G00, G10, G20, G01, G11, G21, G02, G12;
-  if (CX == 0) {
-    const float f4 = 4.0f;
-    G00 = vmul(C.K0, f4); G10 = vmul(C.Ly, f4); G20 = vmul(C.Qyy, f4);
-    G01 = vmul(C.Lz, f4); G11 = vmul(C.Qyz, f4); G21 = vmul(C.Tyyz, f4);
-    G02 = vmul(C.Qzz, f4); G12 = vmul(C.Tyzz, f4);
+  if (CX == 0) {   // (x 1/4)
+    G00 = C.K0; G10 = C.Ly; G20 = C.Qyy;
+    G01 = C.Lz; G11 = C.Qyz; G21 = C.Tyyz;
+    G02 = C.Qzz; G12 = C.Tyzz;
   } else if (CX > 0) {
     G00 = vadd(vadd(C.K0, C.Qxx), C.Lx); G10 = vadd(vadd(C.Ly, C.Txxy), C.Qxy);
     G20 = vadd(C.Qyy, C.Txyy);
@@ -128,21 +138,20 @@ __device__ __forceinline__ void recon_cx(const Coef<V>& C, V (*exch)[kNW][32], i
   for (int cyi = 0; cyi < 3; ++cyi) {
     const int CY = (cyi == 0) ? 1 : (cyi == 1 ? -1 : 0);   // +1, -1, then 0
     V B0, B1, B2;
-    if (CY == 0) {
-      B0 = vmul(G00, 4.0f); B1 = vmul(G01, 4.0f); B2 = vmul(G02, 4.0f);
+    if (CY == 0) {   // (x 1/4)
+      B0 = G00; B1 = G01; B2 = G02;
     } else if (CY > 0) {
       B0 = vadd(vadd(G00, G20), G10); B1 = vadd(vadd(G01, G21), G11); B2 = vadd(G02, G12);
     } else {
       B0 = vsub(vadd(G00, G20), G10); B1 = vsub(vadd(G01, G21), G11); B2 = vsub(G02, G12);
     }
     // cz level: ft(cz=0) = 4 B0, ft(+-1) = (B0 + B2) +- B1
-    const V f0 = vmul(B0, 4.0f);
     const V t = vadd(B0, B2);
     const V fp = vadd(t, B1), fm = vsub(t, B1);
     // z-stage (pull): cz=+1 comes from z-1, cz=-1 from z+1
     const V P = from_zm(fp), M = from_zp(fm);
     const V T2 = vadd(P, M);
-    const V g0 = vadd(f0, T2), g1 = vsub(P, M), g2 = T2;
+    const V g0 = vfma(B0, vsplat(4.0f), T2), g1 = vsub(P, M), g2 = T2;
     if (CY == 0) {
       g0out[0] = g0; g0out[1] = g1; g0out[2] = g2;
     } else {
@@ -256,13 +265,23 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
       }
     }
     V t[10];
+    float lo0 = 1e30f, hi0 = -1e30f, lo1 = 1e30f, hi1 = -1e30f;
 #pragma unroll
     for (int c = 0; c < 10; ++c) {
       t[c] = vfma(s[c], vsplat(A.Q.enc_scale[c]), vsplat(A.Q.enc_off[c]));
+      if (B16) {   // every component maps [min, max] onto [0.5, 65535.5]
+        lo0 = fminf(lo0, t[c].x); hi0 = fmaxf(hi0, t[c].x);
+        lo1 = fminf(lo1, t[c].y); hi1 = fmaxf(hi1, t[c].y);
+      } else {
+        const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+        mx0 = fmaxf(mx0, fabsf(r.x));
+        mx1 = fmaxf(mx1, fabsf(r.y));
+      }
       if (DITHER) t[c] = vadd(t[c], nz[c]);
-      const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
-      mx0 = fmaxf(mx0, fabsf(r.x));
-      mx1 = fmaxf(mx1, fabsf(r.y));
+    }
+    if (B16) {
+      mx0 = (lo0 < 0.5f || hi0 > 65535.5f || hi0 != hi0) ? 2.0f : 0.0f;
+      mx1 = (lo1 < 0.5f || hi1 > 65535.5f || hi1 != hi1) ? 2.0f : 0.0f;
     }
     uint32_t wd[5][2];
 #pragma unroll
@@ -350,7 +369,17 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&S.bar[s], 1);
+      S.stage_cnt[s] = 0;
+    }
+    // y-stage consumers are warps 1..kNW-2; warp v's slots are read by v-1 and v+1
+    for (int b = 0; b < 2; ++b)
+      for (int v = 0; v < kNW; ++v) {
+        mbar_init(&S.full[b][v], 1);
+        const int nc = (v - 1 >= 1 && v - 1 <= kNW - 2) + (v + 1 >= 1 && v + 1 <= kNW - 2);
+        mbar_init(&S.empty[b][v], nc);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
   }
@@ -389,55 +418,77 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     }
     const int sp = (p < 0) ? g.x_lo_src : (p >= g.nx ? g.x_hi_src : p + 1);
     const bool inflow = sp < 0;
-    mbar_wait(&S.bar[it % STAGES], (uint32_t)((it / STAGES) & 1));
+    const int st = it % STAGES;
+    const int b = it & 1;
+    const bool ycons = (w >= 1) && (w <= kNW - 2);   // runs the y-stage (reads both neighbours)
+    mbar_wait(&S.bar[st], (uint32_t)((it / STAGES) & 1));
     V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
     {
       V s[10];
       load_state<Q16>(S.stage[it % STAGES], w, lane, inflow, A, s);
       const Coef<V> C =
           coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+      // the stage has been consumed by this warp (C depends on every loaded value); the last
+      // warp to get here refills it with the plane STAGES iterations ahead
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t old = atomicAdd(&S.stage_cnt[st], 1u);
+        if (old == kNW - 1) {
+          S.stage_cnt[st] = 0;
+          if (it + STAGES < NP)
+            issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, ys0);
+        }
+      }
+      // my slots of buffer b were read by my neighbours two planes ago
+      mbar_wait(&S.empty[b][w], (uint32_t)(((it >> 1) & 1) ^ 1));
       V gz[3];
       // cx = -1 -> dest q (final contribution)
-      recon_cx<-1>(C, exch, w, lane, gz);
-      fin[0] = vadd(A9.a[0], gz[0]);
-      fin[3] = vadd(A9.a[1], gz[1]);
-      fin[9] = vadd(A9.a[2], gz[2]);
+      const V c4 = vsplat(4.0f), cm4 = vsplat(-4.0f), c16 = vsplat(16.0f);
+      recon_cx<-1>(C, exch, w, lane, gz);          // gz at 1/4 scale (cy = 0)
+      fin[0] = vfma(gz[0], c4, A9.a[0]);
+      fin[3] = vfma(gz[1], c4, A9.a[1]);
+      fin[9] = vfma(gz[2], c4, A9.a[2]);
       fin[2] = A9.a[3];
       fin[8] = A9.a[4];
       fin[7] = A9.a[5];
-      fin[1] = vsub(A9.b[0], gz[0]);
-      fin[6] = vsub(A9.b[1], gz[1]);
+      fin[1] = vfma(gz[0], cm4, A9.b[0]);
+      fin[6] = vfma(gz[1], cm4, A9.b[1]);
       fin[5] = A9.b[2];
-      fin[4] = vadd(A9.b[0], gz[0]);
-      // cx = 0 -> dest p
+      fin[4] = vfma(gz[0], c4, A9.b[0]);
+      // cx = 0 -> dest p                          (gz at 1/16 scale: cx = 0 and cy = 0)
       recon_cx<0>(C, exch, w, lane, gz);
       nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
-      nb.a[0] = vadd(B6.a[0], gz[0]);
-      nb.a[1] = vadd(B6.a[1], gz[1]);
-      nb.a[2] = vadd(B6.a[2], gz[2]);
+      nb.a[0] = vfma(gz[0], c16, B6.a[0]);
+      nb.a[1] = vfma(gz[1], c16, B6.a[1]);
+      nb.a[2] = vfma(gz[2], c16, B6.a[2]);
       nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
-      // cx = +1 -> dest p+1
+      // cx = +1 -> dest p+1                       (gz at 1/4 scale, folded after the y-stage)
       recon_cx<1>(C, exch, w, lane, gz);
       nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
     }
-    __syncthreads();   // exch[it&1] complete; every thread is done reading stage it%STAGES
-    if (threadIdx.x == 0 && it + STAGES < NP) {
-      const int j = it + STAGES;
-      issue_plane<NC>(A, xs - 1 + j, S.stage[j % STAGES], &S.bar[j % STAGES], zs0, ys0);
-    }
-    if (row_interior) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.full[b][w]);
+    if (ycons) {
+      mbar_wait(&S.full[b][w - 1], (uint32_t)((it >> 1) & 1));
+      mbar_wait(&S.full[b][w + 1], (uint32_t)((it >> 1) & 1));
       V t[3], d[2];
       ystage<-1>(exch, w, lane, t, d);
       fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
       fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
       fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
       fin[4] = vadd(fin[4], t[0]);
-      ystage<0>(exch, w, lane, t, d);
-      nb.a[0] = vadd(nb.a[0], t[0]); nb.a[1] = vadd(nb.a[1], t[1]); nb.a[2] = vadd(nb.a[2], t[2]);
-      nb.a[3] = vadd(nb.a[3], d[0]); nb.a[4] = vadd(nb.a[4], d[1]); nb.a[5] = vadd(nb.a[5], t[0]);
+      ystage<0>(exch, w, lane, t, d);              // cx = 0 slots are at 1/4 scale
+      const V c4 = vsplat(4.0f);
+      nb.a[0] = vfma(t[0], c4, nb.a[0]); nb.a[1] = vfma(t[1], c4, nb.a[1]); nb.a[2] = vfma(t[2], c4, nb.a[2]);
+      nb.a[3] = vfma(d[0], c4, nb.a[3]); nb.a[4] = vfma(d[1], c4, nb.a[4]); nb.a[5] = vfma(t[0], c4, nb.a[5]);
       ystage<1>(exch, w, lane, t, d);
-      nn.a[0] = vadd(nn.a[0], t[0]); nn.a[1] = vadd(nn.a[1], t[1]); nn.a[2] = vadd(nn.a[2], t[2]);
+      nn.a[0] = vfma(nn.a[0], c4, t[0]); nn.a[1] = vfma(nn.a[1], c4, t[1]); nn.a[2] = vfma(nn.a[2], c4, t[2]);
       nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&S.empty[b][w - 1]);
+        mbar_arrive(&S.empty[b][w + 1]);
+      }
       if (store_plane) {
         const bool sx = A.do_stats && wx && !(SPECIAL && (sbits & 1u));
         const bool sy = A.do_stats && wy && !(SPECIAL && (sbits & 2u));

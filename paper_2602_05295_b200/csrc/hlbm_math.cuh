@@ -82,15 +82,17 @@ template <class T, bool FORCE>
 __device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy,
                                           T nyz, T nzz, const Relax& R) {
   const T one = splat<T>(1.0f);
-  T rho = vadd(d, one);
-  T inv = vrcp(rho);
+  const T rho = vadd(d, one);
+  const T inv = vrcp(rho);
   T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);   // pre-kick u (collision.py:158)
-  // diagonal: X_aa = j_a u_a + (1-s)(n_aa - tr n/3) [+ F_a u_a + cd(2F_a u_a - F_b u_b - F_g u_g)]
-  T q = vmul(vadd(vadd(nxx, nyy), nzz), splat<T>(1.0f / 3.0f));
   const T om = splat<T>(R.om);
-  T Xxx = vfma(jx, ux, vmul(om, vsub(nxx, q)));
-  T Xyy = vfma(jy, uy, vmul(om, vsub(nyy, q)));
-  T Xzz = vfma(jz, uz, vmul(om, vsub(nzz, q)));
+  // X = rho S+: off-diagonal (1-s) sneq_ab + j_a u_b; diagonal j_a u_a + (1-s)(sneq_aa - tr/3)
+  // (collision.py:176-191 with rho S = sneq + j j / rho; the trace relaxes at unit rate)
+  const T q = vmul(vadd(vadd(nxx, nyy), nzz), splat<T>(1.0f / 3.0f));
+  T jux = vmul(jx, ux), juy = vmul(jy, uy), juz = vmul(jz, uz);
+  T Xxx = vfma(om, vsub(nxx, q), jux);
+  T Xyy = vfma(om, vsub(nyy, q), juy);
+  T Xzz = vfma(om, vsub(nzz, q), juz);
   T Xxy = vfma(jx, uy, vmul(om, nxy));
   T Xxz = vfma(jx, uz, vmul(om, nxz));
   T Xyz = vfma(jy, uz, vmul(om, nyz));
@@ -114,31 +116,39 @@ __device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T
     jpy = vfma(half, fy, jy);
     jpz = vfma(half, fz, jz);
     ux = vmul(jpx, inv); uy = vmul(jpy, inv); uz = vmul(jpz, inv);   // u+ for the reconstruction
+    jux = vmul(jpx, ux); juy = vmul(jpy, uy); juz = vmul(jpz, uz);
   }
-  // Y_aab = X_aa u_b + 2 X_ab u_a - 2 j_a u_a u_b ;  Y_xyz = Xxy uz + Xxz uy + Xyz ux - 2 jx uy uz
-  const T two = splat<T>(2.0f);
-  T ax = vsub(Xxx, vmul(two, vmul(jpx, ux)));   // X_aa - 2 j_a u_a
-  T ay = vsub(Xyy, vmul(two, vmul(jpy, uy)));
-  T az = vsub(Xzz, vmul(two, vmul(jpz, uz)));
-  T Yxxy = vfma(ax, uy, vmul(two, vmul(Xxy, ux)));
-  T Yxyy = vfma(ay, ux, vmul(two, vmul(Xxy, uy)));
-  T Yxxz = vfma(ax, uz, vmul(two, vmul(Xxz, ux)));
-  T Yxzz = vfma(az, ux, vmul(two, vmul(Xxz, uz)));
-  T Yyzz = vfma(az, uy, vmul(two, vmul(Xyz, uz)));
-  T Yyyz = vfma(ay, uz, vmul(two, vmul(Xyz, uy)));
-  T Yxyz = vfma(Xxy, uz, vfma(Xxz, uy, vfma(Xyz, ux, vmul(splat<T>(-2.0f), vmul(jpx, vmul(uy, uz))))));
+  // Hermite coefficients, all x 1/216 (moments.py:64-90):
+  //   Q_aa = 4.5 X_aa, Q_ab = 9 X_ab;  T_aab = 13.5 Y_aab with
+  //   Y_aab = X_aa u_b + 2 X_ab u_a - 2 j_a u_a u_b  (T of moments.py:42-52 times rho)
+  //   => T_aab = al_a u_b + Q_ab (3 u_a),  al_a = 13.5 (X_aa - 2 j_a u_a)
   Coef<T> C;
-  // constant: d - (9/2)(1/3) tr X ; linear: 3 j - (27/2)(1/3)(Y..) ; /216 folded in
-  C.K0 = vfma(splat<T>(-1.5f / 216.0f), vadd(vadd(Xxx, Xyy), Xzz), vmul(d, splat<T>(1.0f / 216.0f)));
-  C.Lx = vfma(splat<T>(-4.5f / 216.0f), vadd(Yxyy, Yxzz), vmul(jpx, splat<T>(3.0f / 216.0f)));
-  C.Ly = vfma(splat<T>(-4.5f / 216.0f), vadd(Yxxy, Yyzz), vmul(jpy, splat<T>(3.0f / 216.0f)));
-  C.Lz = vfma(splat<T>(-4.5f / 216.0f), vadd(Yxxz, Yyyz), vmul(jpz, splat<T>(3.0f / 216.0f)));
-  const T q2 = splat<T>(4.5f / 216.0f), q11 = splat<T>(9.0f / 216.0f), t3 = splat<T>(13.5f / 216.0f);
+  const T q2 = splat<T>(4.5f / 216.0f), q11 = splat<T>(9.0f / 216.0f);
   C.Qxx = vmul(q2, Xxx); C.Qyy = vmul(q2, Xyy); C.Qzz = vmul(q2, Xzz);
   C.Qxy = vmul(q11, Xxy); C.Qxz = vmul(q11, Xxz); C.Qyz = vmul(q11, Xyz);
-  C.Txxy = vmul(t3, Yxxy); C.Txyy = vmul(t3, Yxyy); C.Txxz = vmul(t3, Yxxz);
-  C.Txzz = vmul(t3, Yxzz); C.Tyzz = vmul(t3, Yyzz); C.Tyyz = vmul(t3, Yyyz);
-  C.Txyz = vmul(t3, Yxyz);
+  const T m27 = splat<T>(-27.0f / 216.0f), t3 = splat<T>(13.5f / 216.0f);
+  const T alx = vfma(Xxx, t3, vmul(jux, m27));
+  const T aly = vfma(Xyy, t3, vmul(juy, m27));
+  const T alz = vfma(Xzz, t3, vmul(juz, m27));
+  const T three = splat<T>(3.0f);
+  const T u3x = vmul(ux, three), u3y = vmul(uy, three), u3z = vmul(uz, three);
+  C.Txxy = vfma(alx, uy, vmul(C.Qxy, u3x));
+  C.Txyy = vfma(aly, ux, vmul(C.Qxy, u3y));
+  C.Txxz = vfma(alx, uz, vmul(C.Qxz, u3x));
+  C.Txzz = vfma(alz, ux, vmul(C.Qxz, u3z));
+  C.Tyzz = vfma(alz, uy, vmul(C.Qyz, u3z));
+  C.Tyyz = vfma(aly, uz, vmul(C.Qyz, u3y));
+  // T_xyz = 13.5 (Xxy uz + Xxz uy + Xyz ux - 2 jx uy uz) = 1.5 (Qxy uz + Qxz uy + Qyz ux) - 27 jx uy uz
+  const T h15 = splat<T>(0.5f);
+  C.Txyz = vfma(vfma(C.Qxy, u3z, vfma(C.Qxz, u3y, vmul(C.Qyz, u3x))), h15,
+                vmul(vmul(jpx, m27), vmul(uy, uz)));
+  // constant: d - 1.5 tr X = d - (Qxx + Qyy + Qzz)/3 ; linear: 3 j - 4.5(Y..) = 3 j - (T + T)/3
+  const T third = splat<T>(-1.0f / 3.0f);
+  C.K0 = vfma(vadd(vadd(C.Qxx, C.Qyy), C.Qzz), third, vmul(d, splat<T>(1.0f / 216.0f)));
+  const T l3 = splat<T>(3.0f / 216.0f);
+  C.Lx = vfma(vadd(C.Txyy, C.Txzz), third, vmul(jpx, l3));
+  C.Ly = vfma(vadd(C.Txxy, C.Tyzz), third, vmul(jpy, l3));
+  C.Lz = vfma(vadd(C.Txxz, C.Tyyz), third, vmul(jpz, l3));
   return C;
 }
 
