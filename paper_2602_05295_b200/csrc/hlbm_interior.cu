@@ -40,7 +40,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "HLBM_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       " @!p bra HLBM_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -148,10 +148,14 @@ __device__ __forceinline__ void recon_cx(const Coef<V>& C, V (*exch)[kNW][32], i
     // cz level: ft(cz=0) = 4 B0, ft(+-1) = (B0 + B2) +- B1
     const V t = vadd(B0, B2);
     const V fp = vadd(t, B1), fm = vsub(t, B1);
-    // z-stage (pull): cz=+1 comes from z-1, cz=-1 from z+1
-    const V P = from_zm(fp), M = from_zp(fm);
-    const V T2 = vadd(P, M);
-    const V g0 = vfma(B0, vsplat(4.0f), T2), g1 = vsub(P, M), g2 = T2;
+    // z-stage (pull): cz=+1 comes from z-1, cz=-1 from z+1.  Lane pair (z0, z0+1):
+    //   P = (fp(z0-1), fp(z0)) = (up, fp.x),  M = (fm(z0+1), fm(z0+2)) = (fm.y, dn)
+    // formed with scalar adds so no shifted register pair has to be assembled.
+    const float up = __shfl_up_sync(0xffffffffu, fp.y, 1);
+    const float dn = __shfl_down_sync(0xffffffffu, fm.x, 1);
+    const V T2 = make_float2(__fadd_rn(up, fm.y), __fadd_rn(fp.x, dn));
+    const V g1 = make_float2(__fsub_rn(up, fm.y), __fsub_rn(fp.x, dn));
+    const V g0 = vfma(B0, vsplat(4.0f), T2), g2 = T2;
     if (CY == 0) {
       g0out[0] = g0; g0out[1] = g1; g0out[2] = g2;
     } else {
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 // ------------------------------------------------------------------------ host launcher
 template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool B16>
 static cudaError_t launch_t(const StepArgs& A, int nblocks, cudaStream_t st) {
-  constexpr int STAGES = Q16 ? 3 : 2;
+  constexpr int STAGES = Q16 ? 4 : 2;
   constexpr int NC = Q16 ? 5 : 10;
   const size_t smem = sizeof(Smem<NC, STAGES>);
   auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, B16, STAGES>;
