@@ -20,6 +20,7 @@ struct hlbm_ctx {
   hlbm_config cfg{};
   int q16 = 0, NC = 10;
   bool b16 = true;   // every component uses all 16 bits of its slot
+  int qmode = 0;     // interior-kernel codec variant (hlbm_launch.h)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   size_t elem_bytes = 4;
@@ -224,6 +225,13 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
     ctx->Q.sat_a[k] = (float)(1.0 / half);
     ctx->Q.sat_b[k] = (float)((shift - mid) / half);
     ctx->Q.levels[k] = (uint32_t)L;
+  }
+  if (ctx->q16) {
+    static const double dmn[10] = {0.8, -0.6, -0.6, -0.6, -0.1, -0.1, -0.1, -0.1, -0.1, -0.1};
+    static const double dmx[10] = {1.5, 0.6, 0.6, 0.6, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1};
+    bool def = ctx->b16;
+    for (int k = 0; k < 10; ++k) def = def && c.qmin[k] == dmn[k] && c.qmax[k] == dmx[k];
+    ctx->qmode = def ? 2 : (ctx->b16 ? 1 : 0);
   }
   // source-plane map for x = -1 / x = nx
   const int nx = c.nx;
@@ -516,7 +524,7 @@ int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
     const int st = (with_stats && s == nsteps - 1) ? 1 : 0;
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->b16, ctx->stream));
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
     ++ctx->launches;
     if (ctx->nb) {
       CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
@@ -596,7 +604,7 @@ int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->b16, ctx->stream));
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
     ++ctx->launches;
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     if (ctx->nb) {

@@ -181,7 +181,31 @@ __device__ __forceinline__ void ystage(V (*exch)[kNW][32], int w, int lane, V t[
 }
 
 // ---------------------------------------------------------------------------------------
-template <bool Q16>
+// codec constants: QMODE 2 = the default QuantSpec ranges as immediates
+struct DefQ {
+  __host__ __device__ static constexpr double mn(int c) { return c == 0 ? 0.8 : (c < 4 ? -0.6 : -0.1); }
+  __host__ __device__ static constexpr double mx(int c) { return c == 0 ? 1.5 : (c < 4 ? 0.6 : 0.1); }
+  __host__ __device__ static constexpr float dec_step(int c) { return (float)((mx(c) - mn(c)) / 65535.0); }
+  __host__ __device__ static constexpr float dec_off(int c) { return (float)(mn(c) - (c == 0 ? 1.0 : 0.0)); }
+  __host__ __device__ static constexpr float enc_scale(int c) { return (float)(65535.0 / (mx(c) - mn(c))); }
+  __host__ __device__ static constexpr float enc_off(int c) {
+    return (float)(((c == 0 ? 1.0 : 0.0) - mn(c)) * (65535.0 / (mx(c) - mn(c))) + 0.5);
+  }
+};
+template <int QMODE> __device__ __forceinline__ float q_dec_step(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::dec_step(c) : Q.dec_step[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_dec_off(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::dec_off(c) : Q.dec_off[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_enc_scale(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::enc_scale(c) : Q.enc_scale[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_enc_off(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::enc_off(c) : Q.enc_off[c];
+}
+
+template <bool Q16, int QMODE>
 __device__ __forceinline__ void load_state(const uint32_t (*st)[kNW][kZW], int w, int lane,
                                            bool inflow, const StepArgs& A, V s[10]) {
   if (inflow) {
@@ -199,9 +223,10 @@ __device__ __forceinline__ void load_state(const uint32_t (*st)[kNW][kZW], int w
       const uint2 wv = *reinterpret_cast<const uint2*>(&st[k][w][2 * lane]);
       const V lo = make_float2(code_lo_f(wv.x), code_lo_f(wv.y));
       const V hi = make_float2(code_hi_f(wv.x), code_hi_f(wv.y));
-      s[2 * k] = vfma(vsub(lo, two23), vsplat(A.Q.dec_step[2 * k]), vsplat(A.Q.dec_off[2 * k]));
-      s[2 * k + 1] =
-          vfma(vsub(hi, two23), vsplat(A.Q.dec_step[2 * k + 1]), vsplat(A.Q.dec_off[2 * k + 1]));
+      s[2 * k] = vfma(vsub(lo, two23), vsplat(q_dec_step<QMODE>(A.Q, 2 * k)),
+                      vsplat(q_dec_off<QMODE>(A.Q, 2 * k)));
+      s[2 * k + 1] = vfma(vsub(hi, two23), vsplat(q_dec_step<QMODE>(A.Q, 2 * k + 1)),
+                          vsplat(q_dec_off<QMODE>(A.Q, 2 * k + 1)));
     }
   }
 }
@@ -223,7 +248,7 @@ __device__ __forceinline__ void write_images(const Geo& g, E* base_plane, int y,
 
 // store of one finished cell pair + fused statistics.  zs = storage column of the .x cell
 // (even -> 8-byte aligned pair); logical z of .x is zs - 1.
-template <bool Q16, bool DITHER, bool B16>
+template <bool Q16, bool DITHER, int QMODE>
 __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int zs,
                                            bool wx, bool wy, bool statx, bool staty, float red[5]) {
   const Geo& g = A.g;
@@ -234,6 +259,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
   const int zx = zs - 1, zy = zs;
   const bool edge = (y == 0) || (y == g.ny - 1) || (wx && (zx == 0 || zx == g.nz - 1)) ||
                     (wy && (zy == 0 || zy == g.nz - 1));
+  constexpr bool B16 = QMODE >= 1;
   if (!Q16) {
     float* out = reinterpret_cast<float*>(A.out) + off;
     if (wx && wy) {
@@ -272,7 +298,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     float lo0 = 1e30f, hi0 = -1e30f, lo1 = 1e30f, hi1 = -1e30f;
 #pragma unroll
     for (int c = 0; c < 10; ++c) {
-      t[c] = vfma(s[c], vsplat(A.Q.enc_scale[c]), vsplat(A.Q.enc_off[c]));
+      t[c] = vfma(s[c], vsplat(q_enc_scale<QMODE>(A.Q, c)), vsplat(q_enc_off<QMODE>(A.Q, c)));
       if (B16) {   // every component maps [min, max] onto [0.5, 65535.5]
         lo0 = fminf(lo0, t[c].x); hi0 = fmaxf(hi0, t[c].x);
         lo1 = fminf(lo1, t[c].y); hi1 = fmaxf(hi1, t[c].y);
@@ -346,7 +372,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
   }
 }
 
-template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool B16, int STAGES>
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, int QMODE, int STAGES>
 __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_constant__ StepArgs A) {
   constexpr int NC = Q16 ? 5 : 10;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -429,7 +455,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
     {
       V s[10];
-      load_state<Q16>(S.stage[it % STAGES], w, lane, inflow, A, s);
+      load_state<Q16, QMODE>(S.stage[it % STAGES], w, lane, inflow, A, s);
       const Coef<V> C =
           coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
       // the stage has been consumed by this warp (C depends on every loaded value); the last
@@ -496,7 +522,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       if (store_plane) {
         const bool sx = A.do_stats && wx && !(SPECIAL && (sbits & 1u));
         const bool sy = A.do_stats && wy && !(SPECIAL && (sbits & 2u));
-        store_pair<Q16, DITHER, B16>(A, fin, q, yrow, zst, wx, wy, sx, sy, red);
+        store_pair<Q16, DITHER, QMODE>(A, fin, q, yrow, zst, wx, wy, sx, sy, red);
       }
     }
   };
@@ -545,12 +571,12 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 }
 
 // ------------------------------------------------------------------------ host launcher
-template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool B16>
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, int QMODE>
 static cudaError_t launch_t(const StepArgs& A, int nblocks, cudaStream_t st) {
   constexpr int STAGES = Q16 ? 4 : 2;
   constexpr int NC = Q16 ? 5 : 10;
   const size_t smem = sizeof(Smem<NC, STAGES>);
-  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, B16, STAGES>;
+  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, QMODE, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<nblocks, kNW * 32, smem, st>>>(A);
@@ -558,24 +584,23 @@ static cudaError_t launch_t(const StepArgs& A, int nblocks, cudaStream_t st) {
 }
 
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
-                                  bool b16, cudaStream_t st) {
+                                  int qmode, cudaStream_t st) {
   const int nblocks = A.g.nzt * A.g.nyt * A.g.nxs;
   if (nblocks == 0) return cudaSuccess;
 #define HLBM_F(F, S)                                                               \
-  if (!q16 && force == F && special == S) return launch_t<false, F, S, false, false>(A, nblocks, st);
+  if (!q16 && force == F && special == S) return launch_t<false, F, S, false, 0>(A, nblocks, st);
   HLBM_F(false, false) HLBM_F(false, true) HLBM_F(true, false) HLBM_F(true, true)
 #undef HLBM_F
-#define HLBM_Q(F, S, D, B)                                                                     \
-  if (q16 && force == F && special == S && dither == D && b16 == B)                           \
-    return launch_t<true, F, S, D, B>(A, nblocks, st);
-  HLBM_Q(false, false, false, true) HLBM_Q(false, true, false, true)
-  HLBM_Q(true, false, false, true) HLBM_Q(true, true, false, true)
-  HLBM_Q(false, false, true, true) HLBM_Q(false, true, true, true)
-  HLBM_Q(true, false, true, true) HLBM_Q(true, true, true, true)
-  HLBM_Q(false, false, false, false) HLBM_Q(false, true, false, false)
-  HLBM_Q(true, false, false, false) HLBM_Q(true, true, false, false)
-  HLBM_Q(false, false, true, false) HLBM_Q(false, true, true, false)
-  HLBM_Q(true, false, true, false) HLBM_Q(true, true, true, false)
+#define HLBM_Q(F, S, D, M)                                                                     \
+  if (q16 && force == F && special == S && dither == D && qmode == M)                         \
+    return launch_t<true, F, S, D, M>(A, nblocks, st);
+#define HLBM_QM(M)                                                                            \
+  HLBM_Q(false, false, false, M) HLBM_Q(false, true, false, M)                                 \
+  HLBM_Q(true, false, false, M) HLBM_Q(true, true, false, M)                                   \
+  HLBM_Q(false, false, true, M) HLBM_Q(false, true, true, M)                                   \
+  HLBM_Q(true, false, true, M) HLBM_Q(true, true, true, M)
+  HLBM_QM(0) HLBM_QM(1) HLBM_QM(2)
+#undef HLBM_QM
 #undef HLBM_Q
   return cudaErrorInvalidValue;
 }

@@ -13,8 +13,9 @@ struct MaskGeo {
   int bc_ywall_lo, bc_ywall_hi, bc_zwall_lo, bc_zwall_hi;
 };
 
+// qmode: 0 generic bit widths, 1 all 16-bit, 2 all 16-bit with the default QuantSpec ranges
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
-                                  bool b16, cudaStream_t st);
+                                  int qmode, cudaStream_t st);
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
