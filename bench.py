@@ -186,7 +186,7 @@ def _dist_env():
 def _make(precision, world, rank, local):
     from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
     from paper_2602_05295_b200.geometry import turbulence_modes
-    cfg = SolverConfig(nu=1e-4, precision=precision, quant=QuantSpec(), device=local, xseg=128)
+    cfg = SolverConfig(nu=1e-4, precision=precision, quant=QuantSpec(), device=local)
     gdims = (N_PER_GPU * world, N_PER_GPU, N_PER_GPU)
     modes = turbulence_modes(N_PER_GPU, seed=0)
     modes = modes.copy()

@@ -26,6 +26,7 @@ struct hlbm_ctx {
   size_t elem_bytes = 4;
   int64_t plane_elems = 0, total_elems = 0;
   int zp = 0;
+  int num_sms = 148;
   CUtensorMap tmap[2];
   void* buf[2] = {nullptr, nullptr};
   int cur = 0;
@@ -64,6 +65,23 @@ int fail(hlbm_ctx* c, int code, const std::string& msg) {
       return fail(ctx, HLBM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// x-segment length of the interior kernel: each CTA marches xseg planes (+2 re-read planes).
+// Time ~ ceil(blocks / sms) * (xseg + 2); pick the xseg minimising it relative to the work.
+int auto_xseg(int nx, int tiles_yz, int sms) {
+  int best = std::min(nx, 128);
+  double best_cost = 1e30;
+  for (int xs = std::min(nx, 256); xs >= 1; --xs) {
+    const int64_t blocks = (int64_t)tiles_yz * ((nx + xs - 1) / xs);
+    const double waves = std::ceil((double)blocks / sms);
+    const double cost = waves * (xs + 2) * sms / ((double)tiles_yz * nx);
+    if (cost < best_cost * (1.0 - 1e-3)) {
+      best_cost = cost;
+      best = xs;
+    }
+  }
+  return best;
+}
+
 Geo make_geo(const hlbm_ctx* ctx) {
   const hlbm_config& c = ctx->cfg;
   Geo g{};
@@ -75,8 +93,7 @@ Geo make_geo(const hlbm_ctx* ctx) {
   g.x_hi_src = ctx->x_hi_src;
   g.nzt = (c.nz + kZT - 1) / kZT;
   g.nyt = (c.ny + kRows - 1) / kRows;
-  g.xseg = c.xseg > 0 ? c.xseg : 64;
-  if (g.xseg > c.nx) g.xseg = c.nx;
+  g.xseg = c.xseg > 0 ? std::min(c.xseg, c.nx) : auto_xseg(c.nx, g.nzt * g.nyt, ctx->num_sms);
   g.nxs = (c.nx + g.xseg - 1) / g.xseg;
   g.gx0 = c.x0; g.gny = c.gny; g.gnz = c.gnz; g.gnx_total = c.gnx;
   return g;
@@ -194,6 +211,7 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
     }
   }
   if (cudaSetDevice(c.device) != cudaSuccess) return bad("cannot select CUDA device");
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device);
 
   // relaxation constants (collision.py:158-191)
   const double tau = c.tau, s = 1.0 / tau;

@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     const bool store_plane = row_interior && q >= xs && q < xe;
     V (*exch)[kNW][32] = S.exch[it & 1];
     uint32_t sbits = 0;
-    if (SPECIAL && store_plane) {
+    if (SPECIAL && store_plane && (wx || wy)) {   // lanes past the last z cell read nothing
       const int zq = max(zst - 1, 0);   // word holding the pair (z of .x may be -1 at tile 0)
       const int64_t bi = ((int64_t)q * g.ny + yrow) * A.bits_row_words + (zq >> 5);
       const uint32_t wv = __ldg(A.special_bits + bi);
