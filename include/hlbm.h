@@ -68,6 +68,8 @@ typedef struct hlbm_stats {
   int64_t saturation[10];
   int64_t n_fluid;
   int32_t finite;
+  double force[3];             /* triangle mesh: momentum exchange on the solid */
+  double torque[3];
 } hlbm_stats;
 
 const char* hlbm_version(void);
@@ -84,6 +86,17 @@ const char* hlbm_last_error(const hlbm_ctx* ctx);
  * the neighbouring slabs for remote faces (NULL: derived from the x BC).  Builds the sorted
  * boundary-cell list and 27-bit link masks on the device (SPEC.md:400-402 SurfaceMask role). */
 int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, const uint8_t* ghost_hi);
+
+/* Static triangle mesh (lattice coordinates of this slab's global grid): vertices (nv,3) float64,
+ * faces (nf,3) int32; motion = {v[3], omega[3], center[3]} of the rigid body (NULL: at rest).
+ * Precomputes the cut-link list (earliest hit per pull link x -> x - c_i)
+ * and makes the compacted kernel apply the Eq.-8 boundary populations.
+ * Replaces any voxel mask. */
+int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32_t* faces, int64_t nf,
+                  const double* motion);
+int hlbm_set_solid_motion(hlbm_ctx* ctx, const double* motion);
+/* cut links: global cells (sorted), 27-bit masks, t (n,27) float64 (NaN uncut), triangle (n,27) */
+int hlbm_get_cut_links(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, double* t, int32_t* tri, int64_t* n);
 
 /* State in the reference layout: rho (nx,ny,nz), mom (3,nx,ny,nz), stress (6,nx,ny,nz) float64
  * (moments.py:25-39 outputs; MomentSet fields moments.py:136-172). */

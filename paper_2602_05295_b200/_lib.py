@@ -38,6 +38,7 @@ class HlbmStats(C.Structure):
         ("t_fluid_ms", C.c_double), ("t_copy_ms", C.c_double), ("t_solid_ms", C.c_double),
         ("mass", C.c_double), ("momentum", C.c_double * 3), ("max_u", C.c_double),
         ("saturation", C.c_int64 * 10), ("n_fluid", C.c_int64), ("finite", C.c_int32),
+        ("force", C.c_double * 3), ("torque", C.c_double * 3),
     ]
 
 
@@ -51,6 +52,10 @@ SIGNATURES = {
     "hlbm_destroy": (None, [_P]),
     "hlbm_last_error": (C.c_char_p, [_P]),
     "hlbm_set_mask": (C.c_int, [_P, _P, _P, _P]),
+    "hlbm_set_mesh": (C.c_int, [_P, _DP, C.c_int64, C.POINTER(C.c_int32), C.c_int64, _DP]),
+    "hlbm_set_solid_motion": (C.c_int, [_P, _DP]),
+    "hlbm_get_cut_links": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_uint32), _DP,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "hlbm_set_moments": (C.c_int, [_P, _DP, _DP, _DP]),
     "hlbm_get_moments": (C.c_int, [_P, _DP, _DP, _DP]),
     "hlbm_get_moments_box": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

@@ -44,6 +44,8 @@ struct hlbm_ctx {
   int64_t ns = 0;
   uint32_t* d_bits = nullptr;
   int bits_row_words = 0;
+  MeshLinks mesh;                // triangle-mesh cut links (replaces the voxel lists when set)
+  float solid_v[3] = {0, 0, 0}, solid_w[3] = {0, 0, 0}, solid_c[3] = {0, 0, 0};
   int64_t steps = 0;
   int64_t launches = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -119,6 +121,12 @@ StepArgs make_args(hlbm_ctx* ctx, int with_stats) {
   A.step_key = step_key(ctx->steps, ctx->cfg.seed);
   A.do_stats = with_stats;
   A.stats = ctx->d_stats;
+  A.cut_t = ctx->mesh.t32;
+  for (int k = 0; k < 3; ++k) {
+    A.solid_v[k] = ctx->solid_v[k];
+    A.solid_w[k] = ctx->solid_w[k];
+    A.solid_c[k] = ctx->solid_c[k];
+  }
   return A;
 }
 
@@ -147,6 +155,15 @@ int make_tensor_map(hlbm_ctx* ctx, int b) {
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, HLBM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return HLBM_OK;
+}
+
+void free_mesh(hlbm_ctx* ctx) {
+  cudaFree(ctx->mesh.cells);
+  cudaFree(ctx->mesh.masks);
+  cudaFree(ctx->mesh.t64);
+  cudaFree(ctx->mesh.t32);
+  cudaFree(ctx->mesh.tri);
+  ctx->mesh = MeshLinks();
 }
 
 bool has_force(const hlbm_ctx* ctx) {
@@ -295,6 +312,7 @@ void hlbm_destroy(hlbm_ctx* ctx) {
   cudaFree(ctx->d_bmasks);
   cudaFree(ctx->d_scells);
   cudaFree(ctx->d_bits);
+  free_mesh(ctx);
   for (int i = 0; i < 3; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -471,6 +489,7 @@ int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, c
   if ((c.x_lo_remote && !ghost_lo) || (c.x_hi_remote && !ghost_hi))
     return fail(ctx, HLBM_EINVAL, "remote x faces need the neighbour's ghost mask plane");
 
+  free_mesh(ctx);
   cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
   cudaFree(ctx->d_bmasks); ctx->d_bmasks = nullptr;
   cudaFree(ctx->d_scells); ctx->d_scells = nullptr;
@@ -520,6 +539,77 @@ int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, c
   return HLBM_OK;
 }
 
+int hlbm_set_solid_motion(hlbm_ctx* ctx, const double* motion) {
+  if (!ctx) return HLBM_EINVAL;
+  for (int k = 0; k < 3; ++k) {
+    ctx->solid_v[k] = motion ? (float)motion[k] : 0.f;
+    ctx->solid_w[k] = motion ? (float)motion[3 + k] : 0.f;
+    ctx->solid_c[k] = motion ? (float)motion[6 + k] : 0.f;
+  }
+  ctx->solid_c[0] -= (float)ctx->cfg.x0;   // the kernels work in slab-local x
+  return HLBM_OK;
+}
+
+int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32_t* faces, int64_t nf,
+                  const double* motion) {
+  if (!ctx || nv < 0 || nf < 0 || (nv && !vertices) || (nf && !faces)) return fail(ctx, HLBM_EINVAL, "bad mesh");
+  for (int64_t k = 0; k < 3 * nf; ++k)
+    if (faces[k] < 0 || faces[k] >= nv) return fail(ctx, HLBM_EINVAL, "face index out of range");
+  for (int64_t k = 0; k < 3 * nv; ++k)
+    if (!std::isfinite(vertices[k])) return fail(ctx, HLBM_EINVAL, "non-finite vertex");
+  const hlbm_config& c = ctx->cfg;
+  // the mesh replaces any voxel lists
+  cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
+  cudaFree(ctx->d_bmasks); ctx->d_bmasks = nullptr;
+  cudaFree(ctx->d_scells); ctx->d_scells = nullptr;
+  cudaFree(ctx->d_bits); ctx->d_bits = nullptr;
+  ctx->nb = ctx->ns = 0;
+  free_mesh(ctx);
+  hlbm_set_solid_motion(ctx, motion);
+  std::vector<double> V((size_t)3 * nv);
+  for (int64_t k = 0; k < nv; ++k) {
+    V[3 * k] = vertices[3 * k] - (double)c.x0;   // slab-local x
+    V[3 * k + 1] = vertices[3 * k + 1];
+    V[3 * k + 2] = vertices[3 * k + 2];
+  }
+  double* dV = nullptr;
+  int* dF = nullptr;
+  if (nf > 0) {
+    CK(cudaMalloc(&dV, V.size() * 8));
+    CK(cudaMalloc(&dF, (size_t)3 * nf * 4));
+    CK(cudaMemcpy(dV, V.data(), V.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dF, faces, (size_t)3 * nf * 4, cudaMemcpyHostToDevice));
+    CK(build_mesh_links(dV, dF, (int)nf, c.nx, c.ny, c.nz, ctx->mesh, ctx->stream));
+    cudaFree(dV);
+    cudaFree(dF);
+  }
+  if (ctx->mesh.nb > 0) {
+    ctx->bits_row_words = (c.nz + 31) / 32;
+    const int64_t nw = (int64_t)c.nx * c.ny * ctx->bits_row_words;
+    CK(cudaMalloc(&ctx->d_bits, nw * 4));
+    CK(cudaMemsetAsync(ctx->d_bits, 0, nw * 4, ctx->stream));
+    CK(launch_bits_from_list(ctx->mesh.cells, ctx->mesh.nb, c.nz, ctx->bits_row_words, ctx->d_bits, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return HLBM_OK;
+}
+
+int hlbm_get_cut_links(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, double* t, int32_t* tri, int64_t* n) {
+  if (!ctx || !n) return fail(ctx, HLBM_EINVAL, "null argument");
+  const int64_t nb = ctx->mesh.nb;
+  if (!cells) { *n = nb; return HLBM_OK; }
+  if (*n < nb) return fail(ctx, HLBM_EINVAL, "output buffer too small");
+  *n = nb;
+  if (nb == 0) return HLBM_OK;
+  CK(cudaMemcpy(cells, ctx->mesh.cells, nb * 8, cudaMemcpyDeviceToHost));
+  if (masks) CK(cudaMemcpy(masks, ctx->mesh.masks, nb * 4, cudaMemcpyDeviceToHost));
+  if (t) CK(cudaMemcpy(t, ctx->mesh.t64, nb * 27 * 8, cudaMemcpyDeviceToHost));
+  if (tri) CK(cudaMemcpy(tri, ctx->mesh.tri, nb * 27 * 4, cudaMemcpyDeviceToHost));
+  const int64_t off = (int64_t)ctx->cfg.x0 * ctx->cfg.ny * ctx->cfg.nz;
+  for (int64_t i = 0; i < nb; ++i) cells[i] += off;
+  return HLBM_OK;
+}
+
 int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n) {
   if (!ctx || !n) return fail(ctx, HLBM_EINVAL, "null argument");
   if (!cells) { *n = ctx->nb; return HLBM_OK; }
@@ -537,7 +627,7 @@ int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n
 int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
-  const bool special = ctx->nb + ctx->ns > 0;
+  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   for (int s = 0; s < nsteps; ++s) {
     const int st = (with_stats && s == nsteps - 1) ? 1 : 0;
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
@@ -550,6 +640,10 @@ int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
     }
     if (ctx->ns) {
       CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    if (ctx->mesh.nb) {
+      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream));
       ++ctx->launches;
     }
     ctx->cur = 1 - ctx->cur;
@@ -572,6 +666,10 @@ int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
     }
     if (ctx->ns) {
       CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    if (ctx->mesh.nb) {
+      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream));
       ++ctx->launches;
     }
     ctx->cur = 1 - ctx->cur;
@@ -600,6 +698,10 @@ int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {
   s.max_u = std::sqrt((double)mu2);
   for (int k = 0; k < 10; ++k) s.saturation[k] = (int64_t)h.sat[k];
   s.n_fluid = nfluid;
+  for (int k = 0; k < 3; ++k) {
+    s.force[k] = h.force[k];
+    s.torque[k] = h.torque[k];
+  }
   s.finite = std::isfinite(s.mass) && std::isfinite(s.momentum[0]) && std::isfinite(s.momentum[1]) &&
              std::isfinite(s.momentum[2]) && std::isfinite(s.max_u);
   if (out) *out = s;
@@ -615,7 +717,7 @@ int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     return HLBM_OK;
   }
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
-  const bool special = ctx->nb + ctx->ns > 0;
+  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   double tf = 0, ts = 0;
   for (int s = 0; s < nsteps; ++s) {
     const int st = (s == nsteps - 1) ? 1 : 0;
@@ -631,6 +733,10 @@ int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     }
     if (ctx->ns) {
       CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      ++ctx->launches;
+    }
+    if (ctx->mesh.nb) {
+      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream));
       ++ctx->launches;
     }
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));

@@ -49,22 +49,14 @@ __device__ __forceinline__ void load_cell(const StepArgs& A, int sp, int y, int 
   }
 }
 
-// one link of the pull update; accumulates the raw moments of ft into m
-template <int I, bool Q16, bool FORCE>
-__device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z, uint32_t mask,
-                                          float m[10]) {
-  constexpr int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
-  const Geo& g = A.g;
-  const bool bb = (mask >> I) & 1u;
-  const int sx = bb ? x : x - cx;
-  const int sy = bb ? y : y - cy;   // ghost rows/columns hold the periodic images
-  const int sz = bb ? z : z - cz;
-  float s[10];
-  load_cell<Q16>(A, src_plane(g, sx), sy, sz, s);
-  const Coef<float> C = coeffs<float, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-  float E, O;
-  eval_eo<cx, cy, cz, float>(C, E, O);
-  const float ft = bb ? (E - O) : (E + O);
+// per-cell context of the mesh mode (Eq. 8): post-collision state of x
+struct MeshCtx {
+  float rho, d, nxx, nxy, nxz, nyy, nyz, nzz;   // neq part of rho S+ at x: X - j+ j+ / rho
+  const float* t;                               // this cell's 27 hit parameters
+  float F[3], T[3];                              // momentum exchange accumulators
+};
+
+__device__ __forceinline__ void add_moments(float m[10], int cx, int cy, int cz, float ft) {
   m[0] += ft;
   if (cx) m[1] += cx * ft;
   if (cy) m[2] += cy * ft;
@@ -77,17 +69,63 @@ __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z
   if (cz) m[9] += ft;
 }
 
-template <int I, bool Q16, bool FORCE>
+// one link of the pull update; accumulates the raw moments of ft into m
+//   MODE 0: masked links take the half-way bounce-back population f+_opp(i)(x)
+//   MODE 2: masked links take the Eq.-8 boundary population at p = x - t c_i
+template <int I, bool Q16, bool FORCE, int MODE>
+__device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z, uint32_t mask,
+                                          float m[10], MeshCtx& mc) {
+  constexpr int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
+  const Geo& g = A.g;
+  const bool cut = (mask >> I) & 1u;
+  const bool bb = MODE == 0 && cut;
+  const int sx = bb ? x : x - cx;
+  const int sy = bb ? y : y - cy;   // ghost rows/columns hold the periodic images
+  const int sz = bb ? z : z - cz;
+  float s[10];
+  load_cell<Q16>(A, src_plane(g, sx), sy, sz, s);
+  const Coef<float> C = coeffs<float, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+  float E, O;
+  eval_eo<cx, cy, cz, float>(C, E, O);
+  float ft = bb ? (E - O) : (E + O);
+  if (MODE == 2 && cut) {
+    // Eq. 8: rho_p = rho_x, u_p = v + w x (p - c), rho S_p = rho u_p u_p + (rho S_x - rho u_x u_x)
+    const float t = mc.t[I];
+    const float px = (float)x - t * cx, py = (float)y - t * cy, pz = (float)z - t * cz;
+    const float rx = px - A.solid_c[0], ry = py - A.solid_c[1], rz = pz - A.solid_c[2];
+    const float ux = A.solid_v[0] + A.solid_w[1] * rz - A.solid_w[2] * ry;
+    const float uy = A.solid_v[1] + A.solid_w[2] * rx - A.solid_w[0] * rz;
+    const float uz = A.solid_v[2] + A.solid_w[0] * ry - A.solid_w[1] * rx;
+    const float r = mc.rho;
+    const Coef<float> Cp = hermite<float>(mc.d, r * ux, r * uy, r * uz, ux, uy, uz, r * ux * ux + mc.nxx,
+                                          r * ux * uy + mc.nxy, r * ux * uz + mc.nxz, r * uy * uy + mc.nyy,
+                                          r * uy * uz + mc.nyz, r * uz * uz + mc.nzz);
+    float Ep, Op;
+    eval_eo<cx, cy, cz, float>(Cp, Ep, Op);
+    const float fp = Ep + Op;
+    // momentum exchange: Delta P = -(f_p - f_streamed) c_i on the solid
+    const float df = fp - ft;
+    const float dPx = -df * cx, dPy = -df * cy, dPz = -df * cz;
+    mc.F[0] += dPx; mc.F[1] += dPy; mc.F[2] += dPz;
+    mc.T[0] += ry * dPz - rz * dPy;
+    mc.T[1] += rz * dPx - rx * dPz;
+    mc.T[2] += rx * dPy - ry * dPx;
+    ft = fp;
+  }
+  add_moments(m, cx, cy, cz, ft);
+}
+
+template <int I, bool Q16, bool FORCE, int MODE>
 struct PullAll {
   __device__ __forceinline__ static void run(const StepArgs& A, int x, int y, int z, uint32_t mask,
-                                             float m[10]) {
-    pull_link<I, Q16, FORCE>(A, x, y, z, mask, m);
-    PullAll<I + 1, Q16, FORCE>::run(A, x, y, z, mask, m);
+                                             float m[10], MeshCtx& mc) {
+    pull_link<I, Q16, FORCE, MODE>(A, x, y, z, mask, m, mc);
+    PullAll<I + 1, Q16, FORCE, MODE>::run(A, x, y, z, mask, m, mc);
   }
 };
-template <bool Q16, bool FORCE>
-struct PullAll<27, Q16, FORCE> {
-  __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*) {}
+template <bool Q16, bool FORCE, int MODE>
+struct PullAll<27, Q16, FORCE, MODE> {
+  __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*, MeshCtx&) {}
 };
 
 template <typename E>
@@ -165,15 +203,17 @@ __device__ __forceinline__ void flush_stats(const StepArgs& A, float red[5]) {
   }
 }
 
-// mode 0: pull update of listed (or all) fluid cells; mode 1: reset listed solid cells to rest
-template <bool Q16, bool FORCE, bool DITHER>
+// MODE 0: pull update of listed (or all) cells with voxel bounce-back on masked links;
+// MODE 1: reset listed solid cells to rest; MODE 2: mesh links (Eq. 8) + momentum exchange
+template <bool Q16, bool FORCE, bool DITHER, int MODE>
 __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepArgs A,
                                                   const int64_t* __restrict__ cells,
-                                                  const uint32_t* __restrict__ masks, int64_t n,
-                                                  int mode) {
+                                                  const uint32_t* __restrict__ masks, int64_t n) {
   const Geo& g = A.g;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  MeshCtx mc;
+  mc.F[0] = mc.F[1] = mc.F[2] = mc.T[0] = mc.T[1] = mc.T[2] = 0.f;
   if (idx < n) {
     const int64_t cell = cells ? cells[idx] : idx;
     const int64_t yz = (int64_t)g.ny * g.nz;
@@ -181,20 +221,45 @@ __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepAr
     const int64_t r = cell - (int64_t)x * yz;
     const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
     float s[10];
-    if (mode == 1) {
+    if (MODE == 1) {
 #pragma unroll
       for (int c = 0; c < 10; ++c) s[c] = 0.f;
     } else {
       const uint32_t mask = masks ? masks[idx] : 0u;
+      if (MODE == 2) {
+        float o[10];
+        load_cell<Q16>(A, x + 1, y, z, o);
+        const Post<float> P = collide<float, FORCE>(o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7], o[8], o[9], A.R);
+        const float rho = 1.0f + P.d;
+        mc.rho = rho;
+        mc.d = P.d;
+        // rho (S_x - u_x u_x) of the post-collision state
+        mc.nxx = P.Xxx - P.jpx * P.ux; mc.nxy = P.Xxy - P.jpx * P.uy; mc.nxz = P.Xxz - P.jpx * P.uz;
+        mc.nyy = P.Xyy - P.jpy * P.uy; mc.nyz = P.Xyz - P.jpy * P.uz; mc.nzz = P.Xzz - P.jpz * P.uz;
+        mc.t = A.cut_t + idx * 27;
+      }
       float m[10];
 #pragma unroll
       for (int c = 0; c < 10; ++c) m[c] = 0.f;
-      PullAll<0, Q16, FORCE>::run(A, x, y, z, mask, m);
+      PullAll<0, Q16, FORCE, MODE>::run(A, x, y, z, mask, m, mc);
       raw_to_state<float>(m, s);
     }
-    store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && mode == 0, red);
+    store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && MODE != 1, red);
   }
-  if (A.do_stats && mode == 0) flush_stats(A, red);
+  if (A.do_stats && MODE != 1) flush_stats(A, red);
+  if (MODE == 2 && A.do_stats) {
+    float v[6] = {mc.F[0], mc.F[1], mc.F[2], mc.T[0], mc.T[1], mc.T[2]};
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    if ((threadIdx.x & 31) == 0) {
+      for (int k = 0; k < 3; ++k) {
+        atomicAdd(&A.stats->force[k], (double)v[k]);
+        atomicAdd(&A.stats->torque[k], (double)v[3 + k]);
+      }
+    }
+  }
 }
 
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
@@ -205,7 +270,9 @@ cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uin
   const int64_t nb = (n + tpb - 1) / tpb;
 #define HLBM_PULL(Q, F, D)                                                                      \
   if (q16 == Q && force == F && dither == D) {                                                  \
-    pull_cells<Q, F, D><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, mode);               \
+    if (mode == 0) pull_cells<Q, F, D, 0><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);   \
+    else if (mode == 1) pull_cells<Q, F, D, 1><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n); \
+    else pull_cells<Q, F, D, 2><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);             \
     return cudaGetLastError();                                                                  \
   }
   HLBM_PULL(false, false, false)

@@ -14,8 +14,24 @@ struct MaskGeo {
 };
 
 // qmode: 0 generic bit widths, 1 all 16-bit, 2 all 16-bit with the default QuantSpec ranges
+struct MeshLinks {               // cut-link table of a static triangle mesh (device arrays)
+  int64_t* cells = nullptr;      // sorted local linear cell indices
+  uint32_t* masks = nullptr;     // bit i: the pull link x -> x - c_i crosses the mesh
+  double* t64 = nullptr;         // (nb, 27) hit parameter, NaN where uncut (exported)
+  float* t32 = nullptr;          // (nb, 27) the same in float for the step kernel
+  int* tri = nullptr;            // (nb, 27) triangle index, -1 where uncut
+  int64_t nb = 0;
+};
+cudaError_t build_mesh_links(const double* dV, const int* dF, int nf, int nx, int ny, int nz, MeshLinks& out,
+                             cudaStream_t st);
+
+cudaError_t launch_bits_from_list(const int64_t* cells, int64_t n, int nz, int row_words, uint32_t* bits,
+                                  cudaStream_t st);
+
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
                                   int qmode, cudaStream_t st);
+// mode 0: voxel bounce-back on masked links; 1: reset listed solid cells to rest;
+// 2: triangle mesh, Eq.-8 boundary populations on masked links (t table in A.cut_t)
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,

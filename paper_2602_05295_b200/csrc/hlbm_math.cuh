@@ -75,12 +75,59 @@ struct Coef {
   T Txxy, Txyy, Txxz, Txzz, Tyzz, Tyyz, Txyz;
 };
 
-// Post-collision (collision.py:137-194, written in sneq form) and expansion of the
-// third-order Hermite reconstruction (moments.py:64-90) for one (pair of) cell(s).
-//   X = rho S+  (full post-collision stress), Y = rho T (third-order closure, moments.py:42-52)
+// Hermite expansion (moments.py:64-90) of post-collision moments: d = rho - 1, jp = rho u+,
+// up = u+, X = rho S+ (full stress, Voigt xx,xy,xz,yy,yz,zz).
+template <class T>
+__device__ __forceinline__ Coef<T> hermite(T d, T jpx, T jpy, T jpz, T ux, T uy, T uz, T Xxx, T Xxy,
+                                           T Xxz, T Xyy, T Xyz, T Xzz) {
+  const T jux = vmul(jpx, ux), juy = vmul(jpy, uy), juz = vmul(jpz, uz);
+  // Hermite coefficients, all x 1/216 (moments.py:64-90):
+  //   Q_aa = 4.5 X_aa, Q_ab = 9 X_ab;  T_aab = 13.5 Y_aab with
+  //   Y_aab = X_aa u_b + 2 X_ab u_a - 2 j_a u_a u_b  (T of moments.py:42-52 times rho)
+  //   => T_aab = al_a u_b + Q_ab (3 u_a),  al_a = 13.5 (X_aa - 2 j_a u_a)
+  Coef<T> C;
+  const T q2 = splat<T>(4.5f / 216.0f), q11 = splat<T>(9.0f / 216.0f);
+  C.Qxx = vmul(q2, Xxx); C.Qyy = vmul(q2, Xyy); C.Qzz = vmul(q2, Xzz);
+  C.Qxy = vmul(q11, Xxy); C.Qxz = vmul(q11, Xxz); C.Qyz = vmul(q11, Xyz);
+  const T m27 = splat<T>(-27.0f / 216.0f), t3 = splat<T>(13.5f / 216.0f);
+  const T alx = vfma(Xxx, t3, vmul(jux, m27));
+  const T aly = vfma(Xyy, t3, vmul(juy, m27));
+  const T alz = vfma(Xzz, t3, vmul(juz, m27));
+  const T three = splat<T>(3.0f);
+  const T u3x = vmul(ux, three), u3y = vmul(uy, three), u3z = vmul(uz, three);
+  C.Txxy = vfma(alx, uy, vmul(C.Qxy, u3x));
+  C.Txyy = vfma(aly, ux, vmul(C.Qxy, u3y));
+  C.Txxz = vfma(alx, uz, vmul(C.Qxz, u3x));
+  C.Txzz = vfma(alz, ux, vmul(C.Qxz, u3z));
+  C.Tyzz = vfma(alz, uy, vmul(C.Qyz, u3z));
+  C.Tyyz = vfma(aly, uz, vmul(C.Qyz, u3y));
+  // T_xyz = 13.5 (Xxy uz + Xxz uy + Xyz ux - 2 jx uy uz) = 1.5 (Qxy uz + Qxz uy + Qyz ux) - 27 jx uy uz
+  const T h15 = splat<T>(0.5f);
+  C.Txyz = vfma(vfma(C.Qxy, u3z, vfma(C.Qxz, u3y, vmul(C.Qyz, u3x))), h15,
+                vmul(vmul(jpx, m27), vmul(uy, uz)));
+  // constant: d - 1.5 tr X = d - (Qxx + Qyy + Qzz)/3 ; linear: 3 j - 4.5(Y..) = 3 j - (T + T)/3
+  const T third = splat<T>(-1.0f / 3.0f);
+  C.K0 = vfma(vadd(vadd(C.Qxx, C.Qyy), C.Qzz), third, vmul(d, splat<T>(1.0f / 216.0f)));
+  const T l3 = splat<T>(3.0f / 216.0f);
+  C.Lx = vfma(vadd(C.Txyy, C.Txzz), third, vmul(jpx, l3));
+  C.Ly = vfma(vadd(C.Txxy, C.Tyzz), third, vmul(jpy, l3));
+  C.Lz = vfma(vadd(C.Txxz, C.Tyyz), third, vmul(jpz, l3));
+  return C;
+}
+
+
+// post-collision moments of one (pair of) cell(s): d = rho - 1, jp = rho u+ (mom + F/2),
+// u = u+, X = rho S+ (full stress)
+template <class T>
+struct Post {
+  T d, jpx, jpy, jpz, ux, uy, uz, Xxx, Xxy, Xxz, Xyy, Xyz, Xzz;
+};
+
+// Moment-space collision (collision.py:137-194) written in sneq form:
+//   X_ab = (1-s) sneq_ab + j_a u_b (+ force terms), X_aa = j_a u_a + (1-s)(sneq_aa - tr/3) (+ ...)
 template <class T, bool FORCE>
-__device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy,
-                                          T nyz, T nzz, const Relax& R) {
+__device__ __forceinline__ Post<T> collide(T d, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy, T nyz,
+                                           T nzz, const Relax& R) {
   const T one = splat<T>(1.0f);
   const T rho = vadd(d, one);
   const T inv = vrcp(rho);
@@ -118,38 +165,20 @@ __device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T
     ux = vmul(jpx, inv); uy = vmul(jpy, inv); uz = vmul(jpz, inv);   // u+ for the reconstruction
     jux = vmul(jpx, ux); juy = vmul(jpy, uy); juz = vmul(jpz, uz);
   }
-  // Hermite coefficients, all x 1/216 (moments.py:64-90):
-  //   Q_aa = 4.5 X_aa, Q_ab = 9 X_ab;  T_aab = 13.5 Y_aab with
-  //   Y_aab = X_aa u_b + 2 X_ab u_a - 2 j_a u_a u_b  (T of moments.py:42-52 times rho)
-  //   => T_aab = al_a u_b + Q_ab (3 u_a),  al_a = 13.5 (X_aa - 2 j_a u_a)
-  Coef<T> C;
-  const T q2 = splat<T>(4.5f / 216.0f), q11 = splat<T>(9.0f / 216.0f);
-  C.Qxx = vmul(q2, Xxx); C.Qyy = vmul(q2, Xyy); C.Qzz = vmul(q2, Xzz);
-  C.Qxy = vmul(q11, Xxy); C.Qxz = vmul(q11, Xxz); C.Qyz = vmul(q11, Xyz);
-  const T m27 = splat<T>(-27.0f / 216.0f), t3 = splat<T>(13.5f / 216.0f);
-  const T alx = vfma(Xxx, t3, vmul(jux, m27));
-  const T aly = vfma(Xyy, t3, vmul(juy, m27));
-  const T alz = vfma(Xzz, t3, vmul(juz, m27));
-  const T three = splat<T>(3.0f);
-  const T u3x = vmul(ux, three), u3y = vmul(uy, three), u3z = vmul(uz, three);
-  C.Txxy = vfma(alx, uy, vmul(C.Qxy, u3x));
-  C.Txyy = vfma(aly, ux, vmul(C.Qxy, u3y));
-  C.Txxz = vfma(alx, uz, vmul(C.Qxz, u3x));
-  C.Txzz = vfma(alz, ux, vmul(C.Qxz, u3z));
-  C.Tyzz = vfma(alz, uy, vmul(C.Qyz, u3z));
-  C.Tyyz = vfma(aly, uz, vmul(C.Qyz, u3y));
-  // T_xyz = 13.5 (Xxy uz + Xxz uy + Xyz ux - 2 jx uy uz) = 1.5 (Qxy uz + Qxz uy + Qyz ux) - 27 jx uy uz
-  const T h15 = splat<T>(0.5f);
-  C.Txyz = vfma(vfma(C.Qxy, u3z, vfma(C.Qxz, u3y, vmul(C.Qyz, u3x))), h15,
-                vmul(vmul(jpx, m27), vmul(uy, uz)));
-  // constant: d - 1.5 tr X = d - (Qxx + Qyy + Qzz)/3 ; linear: 3 j - 4.5(Y..) = 3 j - (T + T)/3
-  const T third = splat<T>(-1.0f / 3.0f);
-  C.K0 = vfma(vadd(vadd(C.Qxx, C.Qyy), C.Qzz), third, vmul(d, splat<T>(1.0f / 216.0f)));
-  const T l3 = splat<T>(3.0f / 216.0f);
-  C.Lx = vfma(vadd(C.Txyy, C.Txzz), third, vmul(jpx, l3));
-  C.Ly = vfma(vadd(C.Txxy, C.Tyzz), third, vmul(jpy, l3));
-  C.Lz = vfma(vadd(C.Txxz, C.Tyyz), third, vmul(jpz, l3));
-  return C;
+  Post<T> P;
+  P.d = d; P.jpx = jpx; P.jpy = jpy; P.jpz = jpz; P.ux = ux; P.uy = uy; P.uz = uz;
+  P.Xxx = Xxx; P.Xxy = Xxy; P.Xxz = Xxz; P.Xyy = Xyy; P.Xyz = Xyz; P.Xzz = Xzz;
+  (void)jux; (void)juy; (void)juz;
+  return P;
+}
+
+// collision + Hermite expansion: the 17 reconstruction coefficients of the post-collision state
+template <class T, bool FORCE>
+__device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy,
+                                          T nyz, T nzz, const Relax& R) {
+  const Post<T> P = collide<T, FORCE>(d, jx, jy, jz, nxx, nxy, nxz, nyy, nyz, nzz, R);
+  return hermite<T>(P.d, P.jpx, P.jpy, P.jpz, P.ux, P.uy, P.uz, P.Xxx, P.Xxy, P.Xxz, P.Xyy, P.Xyz,
+                    P.Xzz);
 }
 
 // ft_i for one compile-time direction (cx,cy,cz) and sign s = +1 (c) or -1 (-c):

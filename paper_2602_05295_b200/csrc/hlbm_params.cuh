@@ -39,6 +39,8 @@ struct Stats {                 // device-side accumulators (reset by the host pe
   unsigned int max_u2_bits;    // float bits of max |u|^2 (NaN sorts above +inf)
   unsigned int nonfinite;
   unsigned long long sat[10];
+  double force[3];             // momentum exchange on the triangle mesh (mode 2 links)
+  double torque[3];
 };
 
 struct StepArgs {
@@ -54,6 +56,8 @@ struct StepArgs {
   uint32_t step_key;                // dither key for this step
   int do_stats;
   Stats* stats;
+  const float* cut_t;               // mesh mode: (n_list, 27) hit parameters t (p = x - t c_i)
+  float solid_v[3], solid_w[3], solid_c[3];   // rigid-body velocity, angular velocity, centre
 };
 
 // element offset of cell (y, z) of storage plane sp (component 0)

@@ -111,13 +111,16 @@ class StepStats:
     max_u: float
     saturation: np.ndarray
     n_fluid: int
+    force: np.ndarray = None      # triangle mesh: momentum exchange on the solid
+    torque: np.ndarray = None
 
     @classmethod
     def _from_c(cls, s: "_lib.HlbmStats") -> "StepStats":
         return cls(step=int(s.step), t_fluid_ms=s.t_fluid_ms, t_copy_ms=s.t_copy_ms,
                    t_solid_ms=s.t_solid_ms, mass=s.mass, momentum=np.array(list(s.momentum)),
                    max_u=s.max_u, saturation=np.array(list(s.saturation), dtype=np.int64),
-                   n_fluid=int(s.n_fluid))
+                   n_fluid=int(s.n_fluid), force=np.array(list(s.force)),
+                   torque=np.array(list(s.torque)))
 
 
 @dataclass
@@ -207,6 +210,35 @@ class Solver:
                                           None if gl is None else gl.ctypes.data,
                                           None if gh is None else gh.ctypes.data))
         self.grid.mask = m
+
+    def set_mesh(self, vertices, faces, velocity=(0.0, 0.0, 0.0), omega=(0.0, 0.0, 0.0),
+                 center=(0.0, 0.0, 0.0)):
+        """Static triangle mesh in lattice coordinates (global grid): the pull links it cuts take
+        the Eq.-8 boundary populations; replaces any voxel mask."""
+        V = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+        F = np.ascontiguousarray(faces, dtype=np.int32).reshape(-1, 3)
+        motion = np.ascontiguousarray(np.concatenate([velocity, omega, center]), dtype=np.float64)
+        self._chk(self._lib.hlbm_set_mesh(self._ctx, _lib.dptr(V), len(V),
+                                          F.ctypes.data_as(C.POINTER(C.c_int32)), len(F), _lib.dptr(motion)))
+
+    def set_solid_motion(self, velocity=(0.0, 0.0, 0.0), omega=(0.0, 0.0, 0.0), center=(0.0, 0.0, 0.0)):
+        motion = np.ascontiguousarray(np.concatenate([velocity, omega, center]), dtype=np.float64)
+        self._chk(self._lib.hlbm_set_solid_motion(self._ctx, _lib.dptr(motion)))
+
+    def cut_links(self):
+        """(global cells int64, masks uint32, t (n,27) float64 NaN where uncut, tri (n,27) int32)."""
+        n = C.c_int64(0)
+        self._chk(self._lib.hlbm_get_cut_links(self._ctx, None, None, None, None, C.byref(n)))
+        cells = np.empty(n.value, dtype=np.int64)
+        masks = np.empty(n.value, dtype=np.uint32)
+        t = np.empty((n.value, 27), dtype=np.float64)
+        tri = np.empty((n.value, 27), dtype=np.int32)
+        if n.value:
+            self._chk(self._lib.hlbm_get_cut_links(
+                self._ctx, cells.ctypes.data_as(C.POINTER(C.c_int64)),
+                masks.ctypes.data_as(C.POINTER(C.c_uint32)), _lib.dptr(t),
+                tri.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(n)))
+        return cells, masks, t, tri
 
     def set_moments(self, rho, mom, stress):
         nx, ny, nz = self.grid.dims
