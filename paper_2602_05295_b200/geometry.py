@@ -125,3 +125,49 @@ def evaluate_modes(modes, shape, origin=(0, 0, 0), global_dims=None):
         u[1] += ay * s
         u[2] += az * s
     return u
+
+
+def voxel_surface_mesh(mask):
+    """Triangulated boundary of a voxel solid: every solid-voxel face that touches a fluid voxel
+    becomes two triangles on the cube [x-1/2, x+1/2]^3 (cell centres at integer coordinates).
+    Gives million-triangle test meshes comparable to the paper's scanned models."""
+    m = np.asarray(mask, dtype=bool)
+    nx, ny, nz = m.shape
+    verts = []
+    faces = []
+    nv = 0
+    for ax in range(3):
+        for sgn in (-1, 1):
+            nb = np.zeros_like(m)
+            sl_src = [slice(None)] * 3
+            sl_dst = [slice(None)] * 3
+            if sgn > 0:
+                sl_dst[ax] = slice(0, m.shape[ax] - 1)
+                sl_src[ax] = slice(1, None)
+            else:
+                sl_dst[ax] = slice(1, None)
+                sl_src[ax] = slice(0, m.shape[ax] - 1)
+            nb[tuple(sl_dst)] = m[tuple(sl_src)]
+            exposed = m & ~nb
+            idx = np.argwhere(exposed).astype(np.float64)
+            if not len(idx):
+                continue
+            c = idx.copy()
+            c[:, ax] += 0.5 * sgn
+            u = [a for a in range(3) if a != ax]
+            corners = []
+            for du, dv in ((-0.5, -0.5), (0.5, -0.5), (0.5, 0.5), (-0.5, 0.5)):
+                p = c.copy()
+                p[:, u[0]] += du
+                p[:, u[1]] += dv
+                corners.append(p)
+            q = len(idx)
+            verts.append(np.concatenate(corners))          # 4q vertices: corner k of quad j at k*q + j
+            j = np.arange(q)
+            base = nv
+            faces.append(np.stack([base + j, base + q + j, base + 2 * q + j], axis=1))
+            faces.append(np.stack([base + j, base + 2 * q + j, base + 3 * q + j], axis=1))
+            nv += 4 * q
+    if not verts:
+        return np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int32)
+    return np.concatenate(verts), np.concatenate(faces).astype(np.int32)

@@ -18,7 +18,7 @@ import torch
 
 from oracle.step import taylor_green
 from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
-from paper_2602_05295_b200.geometry import sphere_mask, turbulence_modes, vehicle_mask
+from paper_2602_05295_b200.geometry import sphere_mask, turbulence_modes, vehicle_mask, voxel_surface_mesh
 
 
 def timed(s, steps):
@@ -31,9 +31,11 @@ def timed(s, steps):
     return e0.elapsed_time(e1) / steps
 
 
-def run(name, dims, cfg, init, mask=None, steps=50):
+def run(name, dims, cfg, init, mask=None, steps=50, mesh=None):
     t0 = time.perf_counter()
     s = Solver(SimGrid(dims, mask), cfg)
+    if mesh is not None:
+        s.set_mesh(*mesh)
     s.set_stream(torch.cuda.current_stream().cuda_stream)
     setup = time.perf_counter() - t0
     init(s)
@@ -41,11 +43,12 @@ def run(name, dims, cfg, init, mask=None, steps=50):
     ms = timed(s, steps)
     st = s.step(3)              # phase split (events around each kernel) + stats
     cells = int(np.prod(dims))
-    nb = len(s.boundary_cells) if mask is not None else 0
+    nb = len(s.boundary_cells) if mask is not None else (len(s.cut_links()[0]) if mesh is not None else 0)
     out = {"config": name, "dims": list(dims), "precision": cfg.precision, "ms_per_step": round(ms, 4),
            "mlups": round(cells / ms / 1e3, 1), "fluid_mlups": round(st.n_fluid / ms / 1e3, 1),
            "t_fluid_ms": round(st.t_fluid_ms, 4), "t_solid_ms": round(st.t_solid_ms, 4),
-           "boundary_cells": nb, "solid_cells": cells - st.n_fluid, "mask_setup_s": round(setup, 2),
+           "boundary_cells": nb, "solid_cells": cells - st.n_fluid, "setup_s": round(setup, 2),
+           "triangles": 0 if mesh is None else int(len(mesh[1])),
            "max_u": round(st.max_u, 4), "saturation_rho": int(st.saturation[0])}
     s.close()
     print(json.dumps(out), flush=True)
@@ -64,10 +67,17 @@ def main():
     for prec in ("fp32", "q16"):
         run("3 sphere channel", dims, SolverConfig(nu=1e-4, bc=bc, u_in=(0.1, 0, 0), precision=prec),
             uniform(0.1), mask=m)
+    from oracle.mesh import icosphere
+    sph = icosphere((128, 128, 128), 32.0, 5)
+    run("3b sphere channel, triangle mesh", dims, SolverConfig(nu=1e-4, bc=bc, u_in=(0.1, 0, 0), precision="q16"),
+        uniform(0.1), mesh=sph)
     dims = (1000, 400, 400)
     m = vehicle_mask(dims, seed=0)
     run("4 vehicle", dims, SolverConfig(nu=1e-5, bc=bc, u_in=(0.1, 0, 0), precision="q16",
                                         quant=QuantSpec(dither=True)), uniform(0.1), mask=m)
+    mesh = voxel_surface_mesh(m)
+    run("4b vehicle, triangle mesh", dims, SolverConfig(nu=1e-5, bc=bc, u_in=(0.1, 0, 0), precision="q16",
+                                                        quant=QuantSpec(dither=True)), uniform(0.1), mesh=mesh)
 
 
 if __name__ == "__main__":
