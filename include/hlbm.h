@@ -123,6 +123,11 @@ int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n
 /* raw packed words of the q16 state, (5,nx,ny,nz) uint32 (SPEC.md:381 packed-buffer dump) */
 int hlbm_get_codes(hlbm_ctx* ctx, uint32_t* words);
 int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words);
+/* raw internal state, dense (NC,nx,ny,nz) 32-bit words: fp32 (rho-1, rho u, sneq) or q16 words;
+ * with hlbm_set_step_count this is an exact checkpoint/resume */
+int hlbm_get_state(hlbm_ctx* ctx, void* words);
+int hlbm_set_state(hlbm_ctx* ctx, const void* words);
+int hlbm_set_step_count(hlbm_ctx* ctx, int64_t step);
 
 /* multi-GPU plumbing: run on an external stream (e.g. torch's), and expose the device planes
  * that the x-slab halo exchange sends/receives for the CURRENT state buffer. */

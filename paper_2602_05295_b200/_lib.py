@@ -69,6 +69,9 @@ SIGNATURES = {
                                     C.POINTER(C.c_int64)]),
     "hlbm_get_codes": (C.c_int, [_P, C.POINTER(C.c_uint32)]),
     "hlbm_set_codes": (C.c_int, [_P, C.POINTER(C.c_uint32)]),
+    "hlbm_get_state": (C.c_int, [_P, _P]),
+    "hlbm_set_state": (C.c_int, [_P, _P]),
+    "hlbm_set_step_count": (C.c_int, [_P, C.c_int64]),
     "hlbm_set_stream": (C.c_int, [_P, _P]),
     "hlbm_halo_planes": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                                    C.POINTER(C.c_int64)]),

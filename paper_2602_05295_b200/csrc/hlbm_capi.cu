@@ -438,33 +438,49 @@ int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmo
   return HLBM_OK;
 }
 
-int hlbm_get_codes(hlbm_ctx* ctx, uint32_t* words) {
+int hlbm_get_state(hlbm_ctx* ctx, void* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
-  if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
   const hlbm_config& c = ctx->cfg;
-  const int64_t n = (int64_t)5 * c.nx * c.ny * c.nz;
+  const int64_t n = (int64_t)ctx->NC * c.nx * c.ny * c.nz;
   uint32_t* d = nullptr;
   CK(cudaMalloc(&d, n * 4));
-  CK(launch_pack_codes(make_geo(ctx), ctx->buf[ctx->cur], d, 0, ctx->stream));
+  CK(launch_pack_codes(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], d, 0, ctx->stream));
   CK(cudaMemcpyAsync(words, d, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(d);
   return HLBM_OK;
 }
 
-int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words) {
+int hlbm_set_state(hlbm_ctx* ctx, const void* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
-  if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
   const hlbm_config& c = ctx->cfg;
-  const int64_t n = (int64_t)5 * c.nx * c.ny * c.nz;
+  const int64_t n = (int64_t)ctx->NC * c.nx * c.ny * c.nz;
   uint32_t* d = nullptr;
   CK(cudaMalloc(&d, n * 4));
   CK(cudaMemcpyAsync(d, words, n * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(launch_pack_codes(make_geo(ctx), ctx->buf[ctx->cur], d, 1, ctx->stream));
+  CK(launch_pack_codes(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], d, 1, ctx->stream));
   CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(d);
   return HLBM_OK;
+}
+
+int hlbm_set_step_count(hlbm_ctx* ctx, int64_t step) {
+  if (!ctx || step < 0) return fail(ctx, HLBM_EINVAL, "bad step");
+  ctx->steps = step;   // the dither key of the next step (resume from a checkpoint)
+  return HLBM_OK;
+}
+
+int hlbm_get_codes(hlbm_ctx* ctx, uint32_t* words) {
+  if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
+  if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
+  return hlbm_get_state(ctx, words);
+}
+
+int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words) {
+  if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
+  if (!ctx->q16) return fail(ctx, HLBM_EINVAL, "codes exist only for the q16 precision");
+  return hlbm_set_state(ctx, words);
 }
 
 int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, const uint8_t* ghost_hi) {

@@ -583,9 +583,9 @@ __global__ void fill_ghost_rows(Geo g, int NC, uint32_t* buf) {
   }
 }
 
-// interior words of the q16 state <-> dense (5, nx, ny, nz)
-__global__ void pack_codes(Geo g, const uint32_t* __restrict__ buf, uint32_t* __restrict__ dense, int dir) {
-  const int64_t nc = (int64_t)g.nx * g.ny * g.nz, n = 5 * nc;
+// interior words of the state (q16 words or fp32 components) <-> dense (NC, nx, ny, nz)
+__global__ void pack_codes(Geo g, int NC, const uint32_t* __restrict__ buf, uint32_t* __restrict__ dense, int dir) {
+  const int64_t nc = (int64_t)g.nx * g.ny * g.nz, n = NC * nc;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / nc);
@@ -639,9 +639,9 @@ cudaError_t launch_fill_ghosts(const Geo& g, int NC, void* buf, cudaStream_t st)
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_codes(const Geo& g, void* buf, uint32_t* dense, int dir, cudaStream_t st) {
-  const int64_t n = (int64_t)5 * g.nx * g.ny * g.nz;
-  pack_codes<<<grid_for(n, 256), 256, 0, st>>>(g, reinterpret_cast<uint32_t*>(buf), dense, dir);
+cudaError_t launch_pack_codes(const Geo& g, int NC, void* buf, uint32_t* dense, int dir, cudaStream_t st) {
+  const int64_t n = (int64_t)NC * g.nx * g.ny * g.nz;
+  pack_codes<<<grid_for(n, 256), 256, 0, st>>>(g, NC, reinterpret_cast<uint32_t*>(buf), dense, dir);
   return cudaGetLastError();
 }
 

@@ -379,6 +379,24 @@ class Solver:
             raise ValueError("codes must be (5, nx, ny, nz) uint32")
         self._chk(self._lib.hlbm_set_codes(self._ctx, _lib.u32ptr(w)))
 
+    def get_state(self):
+        """Raw internal state (NC, nx, ny, nz): float32 (rho-1, rho u, sneq) or uint32 q16 words."""
+        nx, ny, nz = self.grid.dims
+        q16 = self.config.precision == "q16"
+        w = np.empty((5 if q16 else 10, nx, ny, nz), dtype=np.uint32 if q16 else np.float32)
+        self._chk(self._lib.hlbm_get_state(self._ctx, w.ctypes.data))
+        return w
+
+    def set_state(self, words, step=None):
+        nx, ny, nz = self.grid.dims
+        q16 = self.config.precision == "q16"
+        w = np.ascontiguousarray(words, dtype=np.uint32 if q16 else np.float32)
+        if w.shape != ((5 if q16 else 10), nx, ny, nz):
+            raise ValueError("state shape does not match the grid / precision")
+        self._chk(self._lib.hlbm_set_state(self._ctx, w.ctypes.data))
+        if step is not None:
+            self._chk(self._lib.hlbm_set_step_count(self._ctx, int(step)))
+
     def halo_planes(self):
         """Device pointers (send_lo, send_hi, recv_lo, recv_hi) and bytes per plane."""
         p = [C.c_void_p() for _ in range(4)]
