@@ -69,10 +69,12 @@ int fail(hlbm_ctx* c, int code, const std::string& msg) {
 
 // x-segment length of the interior kernel: each CTA marches xseg planes (+2 re-read planes).
 // Time ~ ceil(blocks / sms) * (xseg + 2); pick the xseg minimising it relative to the work.
+// Segments are capped at 128 planes: longer ones measured slower on B200 (all CTAs of a wave
+// then stream the same few x-planes; fp32 512^3: 3.63 ms at 512 planes vs 2.63 ms at 128).
 int auto_xseg(int nx, int tiles_yz, int sms) {
   int best = std::min(nx, 128);
   double best_cost = 1e30;
-  for (int xs = std::min(nx, 256); xs >= 1; --xs) {
+  for (int xs = std::min(nx, 128); xs >= 1; --xs) {
     const int64_t blocks = (int64_t)tiles_yz * ((nx + xs - 1) / xs);
     const double waves = std::ceil((double)blocks / sms);
     const double cost = waves * (xs + 2) * sms / ((double)tiles_yz * nx);
@@ -148,7 +150,7 @@ int make_tensor_map(hlbm_ctx* ctx, int b) {
   cuuint64_t dims[4] = {(cuuint64_t)ctx->zp, (cuuint64_t)(c.ny + 2), (cuuint64_t)ctx->NC, (cuuint64_t)(c.nx + 2)};
   cuuint64_t strides[3] = {(cuuint64_t)ctx->zp * 4, (cuuint64_t)(c.ny + 2) * ctx->zp * 4,
                            (cuuint64_t)ctx->plane_elems * 4};
-  cuuint32_t box[4] = {(cuuint32_t)kZW, (cuuint32_t)kNW, (cuuint32_t)ctx->NC, 1};
+  cuuint32_t box[4] = {(cuuint32_t)kZW, (cuuint32_t)kBoxRows, (cuuint32_t)ctx->NC, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = encode(&ctx->tmap[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, ctx->buf[b], dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -280,7 +282,7 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
   else ctx->x_hi_src = nx;
 
   ctx->elem_bytes = 4;
-  ctx->zp = (c.nz + 2 + 3) / 4 * 4;
+  ctx->zp = (c.nz + kZOff + 1 + 3) / 4 * 4;   // pad column, z ghosts on both sides
   ctx->plane_elems = (int64_t)ctx->NC * (c.ny + 2) * ctx->zp;
   ctx->total_elems = ctx->plane_elems * (nx + 2);
   *out = ctx;

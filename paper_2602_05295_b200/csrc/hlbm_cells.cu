@@ -136,7 +136,7 @@ __device__ __forceinline__ void put_cell(const Geo& g, E* plane, int y, int z, c
   for (int a = 0; a < 2; ++a)
     for (int b = 0; b < 2; ++b) {
       if ((a && yi == y) || (b && zi == z)) continue;
-      E* p = plane + (int64_t)((a ? yi : y) + 1) * g.zp + ((b ? zi : z) + 1);
+      E* p = plane + (int64_t)((a ? yi : y) + 1) * g.zp + ((b ? zi : z) + kZOff);
       for (int c = 0; c < ncomp; ++c) p[c * g.cstride] = v[c];
     }
 }
@@ -562,14 +562,14 @@ __global__ void fill_ghosts(Geo g, int NC, uint32_t* buf) {
     const int k = (int)(i - pc * 2 * g.ny);
     const int x = (int)(pc / NC), c = (int)(pc - (int64_t)x * NC);
     uint32_t* row = buf + (int64_t)(x + 1) * g.pstride + (int64_t)c * g.cstride + (int64_t)((k >> 1) + 1) * g.zp;
-    if (k & 1) row[g.nz + 1] = row[1];
-    else row[0] = row[g.nz];
+    if (k & 1) row[g.nz + kZOff] = row[kZOff];            // z = nz  <- image of z = 0
+    else row[kZOff - 1] = row[g.nz - 1 + kZOff];         // z = -1  <- image of z = nz-1
   }
 }
 
 // ghost rows (after the columns are filled, so corners are consistent)
 __global__ void fill_ghost_rows(Geo g, int NC, uint32_t* buf) {
-  const int rowsz = g.nz + 2;
+  const int rowsz = g.zp;   // whole padded rows (the z ghost columns included)
   const int64_t n = (int64_t)g.nx * NC * 2 * rowsz;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {

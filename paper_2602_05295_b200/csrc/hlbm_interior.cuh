@@ -1,0 +1,626 @@
+// fluid_interior: the split scheme's divergence-free fluid update (Alg. 2, lines
+// 340-357) over every cell of a slab, sm_100a.
+//
+// Per cell:  load stored moments -> moment-space collision (collision.py:137-194) ->
+// third-order Hermite reconstruction of the 27 post-collision populations (moments.py:64-90)
+// -> pull streaming f_i(x) <- f_i(x - c_i) -> moment extraction
+// (moments.py:25-39) -> neq split (moments.py:93-96) -> store (fp32 or 16-bit codes).
+//
+// Mapping:
+//   * tile = 16 y rows x 60 z cells, marched along x over a segment.  CTA = 16 warps; warp w
+//     owns interior row y0 + w, so every warp stores.  The rows y0-1 and y0+16 outside the
+//     tile only feed populations into it: warps 0 and 15 evaluate just those 9 populations
+//     (cy = +1 resp. -1) of their halo row per plane, a third of a row's reconstruction.
+//   * lane l holds the z pair at storage columns (zs0 + 2l, zs0 + 2l + 1); every arithmetic op
+//     is packed f32x2 (FFMA2/FADD2/FMUL2).  Lanes 1..30 are written (aligned 8-byte pairs:
+//     z = 0 sits at the even storage column kZOff); lanes 0 and 31 are the z halo.
+//   * the x-direction of streaming is a register rotation (two 10-moment accumulators),
+//     never a memory exchange.
+//   * streaming is sum-factorised by axis: z shifts are warp shuffles, y shifts exchange 18
+//     f32x2 per lane through shared memory (neighbour-only mbarrier handshakes, no CTA
+//     barrier), x shifts are the marching accumulators.
+//   * each input plane tile (64 z x 18 y x NC components) is ONE 4-D tensor TMA copy
+//     (cp.async.bulk.tensor + mbarrier) into shared memory, STAGES planes ahead; the y/z ghost
+//     layers of the layout make every tile in-bounds (no wrap).
+#pragma once
+#include "hlbm_params.cuh"
+
+namespace hlbm {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HLBM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HLBM_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ constexpr int slot_of(int cx, int cy, int kz) {
+  return ((cx + 1) * 2 + (cy > 0 ? 0 : 1)) * 3 + kz;
+}
+
+template <int NC, int STAGES, int NB>
+struct Smem {
+  uint32_t stage[STAGES][NC][kBoxRows][kZW];
+  V exch[NB][kNSlot][kNW][32];  // y exchange (NB buffers)
+  V halo[2][9][32];             // halo-row populations: [0] row y0-1 (cy=+1), [1] row y0+16 (cy=-1)
+  uint64_t bar[STAGES];         // TMA stage full (1 arrival + tx bytes)
+  uint64_t full[NB][kNW];       // warp w's exchange slots of buffer b written (1 arrival)
+  uint64_t empty[NB][kNW];      // ... consumed by every y-stage neighbour of w
+  uint32_t stage_cnt[STAGES];   // warps done reading a stage; the last one refills it
+  float red[kNW][5];
+};
+
+// Producer (one thread): the whole plane tile of source plane p is one tensor copy.
+template <int NC>
+__device__ __forceinline__ void issue_plane(const StepArgs& A, int p, uint32_t (*stage)[kBoxRows][kZW],
+                                            uint64_t* bar, int zs0, int ys0) {
+  const Geo& g = A.g;
+  const int sp = (p < 0) ? g.x_lo_src : (p >= g.nx ? g.x_hi_src : p + 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (sp < 0) {   // inflow ghost plane: constants, nothing to load
+    mbar_arrive_expect_tx(bar, 0u);
+    return;
+  }
+  mbar_arrive_expect_tx(bar, (uint32_t)(NC * kBoxRows * kZW * 4));
+  tma_load_4d(&stage[0][0][0], &A.tmap_in, zs0, ys0, 0, sp, bar);
+}
+
+// Partial moments of one destination plane.  Index order of the 6 "kx=0" moments:
+// (ky,kz) = 00, 01, 02, 10, 11, 20.  A plane that has received the cx=+1 contribution
+// of source q-1 and the cx=0 contribution of source q carries 9 values (a: kx=0,
+// b: kx=1 for (ky,kz) = 00, 01, 10; the kx=2 partial equals b[0]).
+struct Part9 {
+  V a[6];
+  V b[3];
+};
+struct Part6 {   // only the cx=+1 contribution of source q-1: kx=1/kx=2 partials are copies
+  V a[6];
+};
+
+// ---------------------------------------------------------------------------------------
+// Nodal evaluation of the reconstruction polynomial, by axis (weights folded as omega(0) = 4,
+// omega(+-1) = 1; centre weights are applied by the consumers' FMAs: the cx = 0 branch runs at
+// 1/4 scale and the cy = 0 results at 1/4 scale.  Scaling by a power of two commutes with
+// rounding, so the results are bit-identical to the unscaled evaluation).
+struct GLev {   // cx level: polynomial in (cy, cz) at the given cx
+  V G00, G10, G20, G01, G11, G21, G02, G12;
+};
+template <int CX>
+__device__ __forceinline__ GLev glevel(const Coef<V>& C) {
+  GLev G;
+  if (CX == 0) {   // (x 1/4)
+    G.G00 = C.K0; G.G10 = C.Ly; G.G20 = C.Qyy;
+    G.G01 = C.Lz; G.G11 = C.Qyz; G.G21 = C.Tyyz;
+    G.G02 = C.Qzz; G.G12 = C.Tyzz;
+  } else if (CX > 0) {
+    G.G00 = vadd(vadd(C.K0, C.Qxx), C.Lx); G.G10 = vadd(vadd(C.Ly, C.Txxy), C.Qxy);
+    G.G20 = vadd(C.Qyy, C.Txyy);
+    G.G01 = vadd(vadd(C.Lz, C.Txxz), C.Qxz); G.G11 = vadd(C.Qyz, C.Txyz); G.G21 = C.Tyyz;
+    G.G02 = vadd(C.Qzz, C.Txzz); G.G12 = C.Tyzz;
+  } else {
+    G.G00 = vsub(vadd(C.K0, C.Qxx), C.Lx); G.G10 = vsub(vadd(C.Ly, C.Txxy), C.Qxy);
+    G.G20 = vsub(C.Qyy, C.Txyy);
+    G.G01 = vsub(vadd(C.Lz, C.Txxz), C.Qxz); G.G11 = vsub(C.Qyz, C.Txyz); G.G21 = C.Tyyz;
+    G.G02 = vsub(C.Qzz, C.Txzz); G.G12 = C.Tyzz;
+  }
+  return G;
+}
+
+// cy level + z-stage: the z-moments (kz = 0, 1, 2) of the three populations (CX, CY, cz)
+// pulled into this lane's cells.  cz level: ft(0) = 4 B0, ft(+-1) = (B0 + B2) +- B1.
+template <int CY>
+__device__ __forceinline__ void zlevel(const GLev& G, V& g0, V& g1, V& g2) {
+  V B0, B1, B2;
+  if (CY == 0) {   // (x 1/4)
+    B0 = G.G00; B1 = G.G01; B2 = G.G02;
+  } else if (CY > 0) {
+    B0 = vadd(vadd(G.G00, G.G20), G.G10); B1 = vadd(vadd(G.G01, G.G21), G.G11); B2 = vadd(G.G02, G.G12);
+  } else {
+    B0 = vsub(vadd(G.G00, G.G20), G.G10); B1 = vsub(vadd(G.G01, G.G21), G.G11); B2 = vsub(G.G02, G.G12);
+  }
+  const V t = vadd(B0, B2);
+  const V fp = vadd(t, B1), fm = vsub(t, B1);
+  // pull: cz=+1 comes from z-1, cz=-1 from z+1.  Lane pair (z0, z0+1):
+  //   P = (fp(z0-1), fp(z0)) = (up, fp.x),  M = (fm(z0+1), fm(z0+2)) = (fm.y, dn)
+  // formed with scalar adds so no shifted register pair has to be assembled.
+  const float up = __shfl_up_sync(0xffffffffu, fp.y, 1);
+  const float dn = __shfl_down_sync(0xffffffffu, fm.x, 1);
+  const V T2 = make_float2(__fadd_rn(up, fm.y), __fadd_rn(fp.x, dn));
+  g1 = make_float2(__fsub_rn(up, fm.y), __fsub_rn(fp.x, dn));
+  g0 = vfma(B0, vsplat(4.0f), T2);
+  g2 = T2;
+}
+
+// own row, one cx: cy = +-1 results to the exchange, cy = 0 results returned
+template <int CX>
+__device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane, V gz[3]) {
+  const GLev G = glevel<CX>(C);
+  V a, b, c;
+  zlevel<1>(G, a, b, c);
+  exch[slot_of(CX, 1, 0)][w][lane] = a;
+  exch[slot_of(CX, 1, 1)][w][lane] = b;
+  exch[slot_of(CX, 1, 2)][w][lane] = c;
+  zlevel<-1>(G, a, b, c);
+  exch[slot_of(CX, -1, 0)][w][lane] = a;
+  exch[slot_of(CX, -1, 1)][w][lane] = b;
+  exch[slot_of(CX, -1, 2)][w][lane] = c;
+  zlevel<0>(G, gz[0], gz[1], gz[2]);
+}
+
+// halo row: only the populations that enter the tile (cy = CY), for every cx
+template <int CY>
+__device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*hs)[32], int lane) {
+  V a, b, c;
+  { const GLev G = glevel<-1>(C); zlevel<CY>(G, a, b, c); hs[0][lane] = a; hs[1][lane] = b; hs[2][lane] = c; }
+  { const GLev G = glevel<0>(C);  zlevel<CY>(G, a, b, c); hs[3][lane] = a; hs[4][lane] = b; hs[5][lane] = c; }
+  { const GLev G = glevel<1>(C);  zlevel<CY>(G, a, b, c); hs[6][lane] = a; hs[7][lane] = b; hs[8][lane] = c; }
+}
+
+// y-stage for one cx: neighbour contributions (row y-1 sent cy=+1, row y+1 sent cy=-1)
+// as t = A + B (even in cy) and d = A - B (odd in cy), per kz.
+template <int CX>
+__device__ __forceinline__ void ystage(V (*exch)[kNW][32], const V (*halo)[9][32], int w, int lane, V t[3],
+                                       V d[2]) {
+  V A0, A1, A2, B0, B1, B2;
+  if (w == 0) {
+    A0 = halo[0][(CX + 1) * 3 + 0][lane]; A1 = halo[0][(CX + 1) * 3 + 1][lane]; A2 = halo[0][(CX + 1) * 3 + 2][lane];
+  } else {
+    A0 = exch[slot_of(CX, 1, 0)][w - 1][lane]; A1 = exch[slot_of(CX, 1, 1)][w - 1][lane];
+    A2 = exch[slot_of(CX, 1, 2)][w - 1][lane];
+  }
+  if (w == kNW - 1) {
+    B0 = halo[1][(CX + 1) * 3 + 0][lane]; B1 = halo[1][(CX + 1) * 3 + 1][lane]; B2 = halo[1][(CX + 1) * 3 + 2][lane];
+  } else {
+    B0 = exch[slot_of(CX, -1, 0)][w + 1][lane]; B1 = exch[slot_of(CX, -1, 1)][w + 1][lane];
+    B2 = exch[slot_of(CX, -1, 2)][w + 1][lane];
+  }
+  t[0] = vadd(A0, B0); t[1] = vadd(A1, B1); t[2] = vadd(A2, B2);
+  d[0] = vsub(A0, B0); d[1] = vsub(A1, B1);
+}
+
+// ---------------------------------------------------------------------------------------
+// codec constants: QMODE 2 = the default QuantSpec ranges as immediates
+struct DefQ {
+  __host__ __device__ static constexpr double mn(int c) { return c == 0 ? 0.8 : (c < 4 ? -0.6 : -0.1); }
+  __host__ __device__ static constexpr double mx(int c) { return c == 0 ? 1.5 : (c < 4 ? 0.6 : 0.1); }
+  __host__ __device__ static constexpr float dec_step(int c) { return (float)((mx(c) - mn(c)) / 65535.0); }
+  __host__ __device__ static constexpr float dec_off(int c) { return (float)(mn(c) - (c == 0 ? 1.0 : 0.0)); }
+  __host__ __device__ static constexpr float enc_scale(int c) { return (float)(65535.0 / (mx(c) - mn(c))); }
+  __host__ __device__ static constexpr float enc_off(int c) {
+    return (float)(((c == 0 ? 1.0 : 0.0) - mn(c)) * (65535.0 / (mx(c) - mn(c))) + 0.5);
+  }
+};
+template <int QMODE> __device__ __forceinline__ float q_dec_step(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::dec_step(c) : Q.dec_step[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_dec_off(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::dec_off(c) : Q.dec_off[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_enc_scale(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::enc_scale(c) : Q.enc_scale[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_enc_off(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::enc_off(c) : Q.enc_off[c];
+}
+
+template <bool Q16, int QMODE>
+__device__ __forceinline__ void load_state(const uint32_t (*st)[kBoxRows][kZW], int row, int lane,
+                                           bool inflow, const StepArgs& A, V s[10]) {
+  if (inflow) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s[c] = vsplat(A.inflow[c]);
+    return;
+  }
+  if (!Q16) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s[c] = *reinterpret_cast<const V*>(&st[c][row][2 * lane]);
+  } else {
+    const V two23 = vsplat(8388608.0f);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint2 wv = *reinterpret_cast<const uint2*>(&st[k][row][2 * lane]);
+      const V lo = make_float2(code_lo_f(wv.x), code_lo_f(wv.y));
+      const V hi = make_float2(code_hi_f(wv.x), code_hi_f(wv.y));
+      s[2 * k] = vfma(vsub(lo, two23), vsplat(q_dec_step<QMODE>(A.Q, 2 * k)),
+                      vsplat(q_dec_off<QMODE>(A.Q, 2 * k)));
+      s[2 * k + 1] = vfma(vsub(hi, two23), vsplat(q_dec_step<QMODE>(A.Q, 2 * k + 1)),
+                          vsplat(q_dec_off<QMODE>(A.Q, 2 * k + 1)));
+    }
+  }
+}
+
+// a finished cell pair (z even, z+1) of row y into plane_base (component 0 of the plane), plus
+// its periodic images in the y/z ghost layers when the pair touches an edge.  E: element type
+// of the layout (float / uint32_t), W: the pair type stored (8 bytes, aligned: z + kZOff even).
+template <typename E, typename W>
+__device__ __forceinline__ void put_pair(const Geo& g, E* plane_base, int y, int z, const W* vals, int ncomp) {
+  E* p = plane_base + (int64_t)(y + 1) * g.zp + (z + kZOff);
+  for (int c = 0; c < ncomp; ++c) *reinterpret_cast<W*>(p + c * g.cstride) = vals[c];
+  const bool ye = (y == 0) || (y == g.ny - 1), ze = (z == 0) || (z == g.nz - 2);
+  if (ye || ze) {
+    const int yi = y == 0 ? g.ny : (y == g.ny - 1 ? -1 : y);
+    const int zi = z == 0 ? g.nz : (z == g.nz - 2 ? -2 : z);   // image pair start (pad column included)
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        if ((a == 0 && b == 0) || (a && !ye) || (b && !ze)) continue;
+        E* q = plane_base + (int64_t)((a ? yi : y) + 1) * g.zp + ((b ? zi : z) + kZOff);
+        for (int c = 0; c < ncomp; ++c) *reinterpret_cast<W*>(q + c * g.cstride) = vals[c];
+      }
+  }
+}
+
+// store of one finished cell pair + fused statistics; z = logical z of the .x cell (even)
+template <bool Q16, bool DITHER, bool STATS, int QMODE>
+__device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z, bool statx,
+                                           bool staty, float red[5]) {
+  const Geo& g = A.g;
+  V s[10];
+  raw_to_state(m, s);
+  const int64_t plane_off = (int64_t)(q + 1) * g.pstride;
+  constexpr bool B16 = QMODE >= 1;
+  if (!Q16) {
+    put_pair(g, reinterpret_cast<float*>(A.out) + plane_off, y, z, s, 10);
+  } else {
+    V nz[10];
+    if (DITHER) {
+      const uint32_t gi = (uint32_t)(((int64_t)(g.gx0 + q) * g.gny + y) * g.gnz + z);
+      const uint32_t h0a = mix32(gi + A.step_key), h0b = mix32(gi + 1u + A.step_key);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const uint32_t kk = (uint32_t)(k + 1) * 0x9E3779B9u;
+        const uint32_t ha = mix32(h0a ^ kk), hb = mix32(h0b ^ kk);
+        nz[2 * k] = make_float2(noise16(ha & 0xFFFFu), noise16(hb & 0xFFFFu));
+        nz[2 * k + 1] = make_float2(noise16(ha >> 16), noise16(hb >> 16));
+      }
+    }
+    V t[10];
+    float lo0 = 1e30f, hi0 = -1e30f, lo1 = 1e30f, hi1 = -1e30f;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) {
+      t[c] = vfma(s[c], vsplat(q_enc_scale<QMODE>(A.Q, c)), vsplat(q_enc_off<QMODE>(A.Q, c)));
+      if (STATS && B16) {   // every component maps [min, max] onto [0.5, 65535.5]
+        lo0 = fminf(lo0, t[c].x); hi0 = fmaxf(hi0, t[c].x);
+        lo1 = fminf(lo1, t[c].y); hi1 = fmaxf(hi1, t[c].y);
+      }
+      if (DITHER) t[c] = vadd(t[c], nz[c]);
+    }
+    uint2 wd[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (B16) {   // 16-bit slots: the saturating cvt is the clamp
+        wd[k].x = pack2_u16_floor(t[2 * k].x, t[2 * k + 1].x);
+        wd[k].y = pack2_u16_floor(t[2 * k].y, t[2 * k + 1].y);
+      } else {
+        const uint32_t a0 = min(f2u16_floor(t[2 * k].x), A.Q.levels[2 * k]);
+        const uint32_t b0 = min(f2u16_floor(t[2 * k + 1].x), A.Q.levels[2 * k + 1]);
+        const uint32_t a1 = min(f2u16_floor(t[2 * k].y), A.Q.levels[2 * k]);
+        const uint32_t b1 = min(f2u16_floor(t[2 * k + 1].y), A.Q.levels[2 * k + 1]);
+        wd[k].x = __byte_perm(a0, b0, 0x5410);
+        wd[k].y = __byte_perm(a1, b1, 0x5410);
+      }
+    }
+    put_pair(g, reinterpret_cast<uint32_t*>(A.out) + plane_off, y, z, wd, 5);
+    if (STATS) {
+      // saturation: |r| > 1  <=>  m outside [min, max]  (rare slow path)
+      bool satx, saty;
+      if (B16) {
+        satx = statx && (lo0 < 0.5f || hi0 > 65535.5f || hi0 != hi0);
+        saty = staty && (lo1 < 0.5f || hi1 > 65535.5f || hi1 != hi1);
+      } else {
+        float mx0 = 0.f, mx1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+          mx0 = fmaxf(mx0, fabsf(r.x));
+          mx1 = fmaxf(mx1, fabsf(r.y));
+        }
+        satx = statx && !(mx0 <= 1.0f);
+        saty = staty && !(mx1 <= 1.0f);
+      }
+      if (satx || saty) {
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+          const unsigned n = (satx && !(fabsf(r.x) <= 1.0f)) + (saty && !(fabsf(r.y) <= 1.0f));
+          if (n) atomicAdd(&A.stats->sat[c], (unsigned long long)n);
+        }
+      }
+    }
+  }
+  if (STATS) {
+    if (statx) {
+      red[0] += s[0].x; red[1] += s[1].x; red[2] += s[2].x; red[3] += s[3].x;
+      const float inv = rcp_nr(1.0f + s[0].x);
+      const float u2 = (s[1].x * s[1].x + s[2].x * s[2].x + s[3].x * s[3].x) * inv * inv;
+      red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
+    }
+    if (staty) {
+      red[0] += s[0].y; red[1] += s[1].y; red[2] += s[2].y; red[3] += s[3].y;
+      const float inv = rcp_nr(1.0f + s[0].y);
+      const float u2 = (s[1].y * s[1].y + s[2].y * s[2].y + s[3].y * s[3].y) * inv * inv;
+      red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
+    }
+  }
+}
+
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE, int STAGES, int NB>
+__global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_constant__ StepArgs A) {
+  constexpr int NC = Q16 ? 5 : 10;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem<NC, STAGES, NB>& S = *reinterpret_cast<Smem<NC, STAGES, NB>*>(smem_raw);
+  const Geo& g = A.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+  int item = blockIdx.x;
+  const int zt = item % g.nzt;
+  item /= g.nzt;
+  const int yt = item % g.nyt;
+  const int xsi = item / g.nyt;
+  const int zs0 = zt * kZT;                 // storage column of the window start
+  const int y0 = yt * kRows;                // first interior row; the box starts at storage row y0
+  const int yrow = y0 + w;                  // logical y of this warp's row
+  const int zc = zs0 - kZOff + 2 * lane;    // logical z of this lane's .x cell (even)
+  const bool wr = (yrow < g.ny) && (lane >= 1) && (lane <= 30) && (zc < g.nz);
+  const int xs = xsi * g.xseg, xe = min(xs + g.xseg, g.nx);
+  const int NP = xe - xs + 2;
+  const bool lo_inflow = g.x_lo_src < 0, hi_inflow = g.x_hi_src < 0;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&S.bar[s], 1);
+      S.stage_cnt[s] = 0;
+    }
+    // warp v's slots are read by its neighbours v-1 and v+1 inside the tile
+    for (int b = 0; b < NB; ++b)
+      for (int v = 0; v < kNW; ++v) {
+        mbar_init(&S.full[b][v], 1);
+        mbar_init(&S.empty[b][v], (v > 0) + (v < kNW - 1));
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int it = 0; it < STAGES && it < NP; ++it)
+      issue_plane<NC>(A, xs - 1 + it, S.stage[it], &S.bar[it], zs0, y0);
+  }
+
+  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  Part9 Ac, Ad;   // dest p-1 partials (two register sets: the loop is unrolled x2)
+  Part6 Bc, Bd;   // dest p partials
+#pragma unroll
+  for (int k = 0; k < 6; ++k) Ac.a[k] = Bc.a[k] = vsplat(0.f);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
+  int st = 0;
+  uint32_t sph = 0;
+
+  // one source plane: (A9, B6) carried in, (nb, nn) carried out
+  auto body = [&](const int it, const Part9& A9, const Part6& B6, Part9& nb, Part6& nn) {
+    const int p = xs - 1 + it;
+    const int q = p - 1;   // destination plane finished in this iteration
+    const bool store_plane = wr && it >= 2;
+    const int b = (NB == 2) ? (it & 1) : 0;
+    const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
+    V (*exch)[kNW][32] = S.exch[b];
+    const bool inflow = (p < 0 && lo_inflow) || (p >= g.nx && hi_inflow);
+    mbar_wait(&S.bar[st], sph);
+    // halo rows: the 9 populations of row y0-1 (cy = +1) / y0+16 (cy = -1) entering the tile
+    if (w == 0 || w == kNW - 1) {
+      V s[10];
+      load_state<Q16, QMODE>(S.stage[st], w == 0 ? 0 : kBoxRows - 1, lane, inflow, A, s);
+      const Coef<V> C =
+          coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+      if (w == 0) recon_halo<1>(C, S.halo[0], lane);
+      else recon_halo<-1>(C, S.halo[1], lane);
+    }
+    V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
+    {
+      V s[10];
+      load_state<Q16, QMODE>(S.stage[st], w + 1, lane, inflow, A, s);
+      const Coef<V> C =
+          coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+      // the stage has been consumed by this warp (C depends on every loaded value); the last
+      // warp to get here refills it with the plane STAGES iterations ahead
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t old = atomicAdd(&S.stage_cnt[st], 1u);
+        if (old == kNW - 1) {
+          S.stage_cnt[st] = 0;
+          if (it + STAGES < NP) issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, y0);
+        }
+      }
+      // my slots of buffer b were read by my neighbours NB planes ago
+      mbar_wait(&S.empty[b][w], eph ^ 1u);
+      V gz[3];
+      // cx = -1 -> dest q (final contribution)
+      const V c4 = vsplat(4.0f), cm4 = vsplat(-4.0f), c16 = vsplat(16.0f);
+      recon_row<-1>(C, exch, w, lane, gz);          // gz at 1/4 scale (cy = 0)
+      fin[0] = vfma(gz[0], c4, A9.a[0]);
+      fin[3] = vfma(gz[1], c4, A9.a[1]);
+      fin[9] = vfma(gz[2], c4, A9.a[2]);
+      fin[2] = A9.a[3];
+      fin[8] = A9.a[4];
+      fin[7] = A9.a[5];
+      fin[1] = vfma(gz[0], cm4, A9.b[0]);
+      fin[6] = vfma(gz[1], cm4, A9.b[1]);
+      fin[5] = A9.b[2];
+      fin[4] = vfma(gz[0], c4, A9.b[0]);
+      // cx = 0 -> dest p                          (gz at 1/16 scale: cx = 0 and cy = 0)
+      recon_row<0>(C, exch, w, lane, gz);
+      nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
+      nb.a[0] = vfma(gz[0], c16, B6.a[0]);
+      nb.a[1] = vfma(gz[1], c16, B6.a[1]);
+      nb.a[2] = vfma(gz[2], c16, B6.a[2]);
+      nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
+      // cx = +1 -> dest p+1                       (gz at 1/4 scale, folded after the y-stage)
+      recon_row<1>(C, exch, w, lane, gz);
+      nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
+    }
+    if (++st == STAGES) { st = 0; sph ^= 1u; }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.full[b][w]);
+    if (w > 0) mbar_wait(&S.full[b][w - 1], eph);
+    if (w < kNW - 1) mbar_wait(&S.full[b][w + 1], eph);
+    {
+      V t[3], d[2];
+      ystage<-1>(exch, S.halo, w, lane, t, d);
+      fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
+      fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
+      fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
+      fin[4] = vadd(fin[4], t[0]);
+      ystage<0>(exch, S.halo, w, lane, t, d);       // cx = 0 slots are at 1/4 scale
+      const V c4 = vsplat(4.0f);
+      nb.a[0] = vfma(t[0], c4, nb.a[0]); nb.a[1] = vfma(t[1], c4, nb.a[1]); nb.a[2] = vfma(t[2], c4, nb.a[2]);
+      nb.a[3] = vfma(d[0], c4, nb.a[3]); nb.a[4] = vfma(d[1], c4, nb.a[4]); nb.a[5] = vfma(t[0], c4, nb.a[5]);
+      ystage<1>(exch, S.halo, w, lane, t, d);
+      nn.a[0] = vfma(nn.a[0], c4, t[0]); nn.a[1] = vfma(nn.a[1], c4, t[1]); nn.a[2] = vfma(nn.a[2], c4, t[2]);
+      nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (w > 0) mbar_arrive(&S.empty[b][w - 1]);
+      if (w < kNW - 1) mbar_arrive(&S.empty[b][w + 1]);
+    }
+    if (store_plane) {
+      bool sx = STATS, sy = STATS;
+      if (STATS && SPECIAL) {   // boundary / solid cells are finished by the compacted kernels
+        const uint32_t wv =
+            __ldg(A.special_bits + ((int64_t)q * g.ny + yrow) * A.bits_row_words + (zc >> 5));
+        sx = !((wv >> (zc & 31)) & 1u);
+        sy = !((wv >> ((zc & 31) + 1)) & 1u);
+      }
+      store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, sx, sy, red);
+    }
+  };
+
+  for (int it = 0; it < NP; it += 2) {
+    body(it, Ac, Bc, Ad, Bd);
+    if (it + 1 < NP) body(it + 1, Ad, Bd, Ac, Bc);
+  }
+
+  if (STATS) {
+    // block reduction of the fused statistics
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float v = red[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      red[k] = v;
+    }
+    float m = red[4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float t = __shfl_xor_sync(0xffffffffu, m, o);
+      m = (t > m || t != t) ? t : m;
+    }
+    red[4] = m;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) S.red[w][k] = red[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a[4] = {0, 0, 0, 0};
+      float mm = 0.f;
+      for (int i = 0; i < kNW; ++i) {
+        for (int k = 0; k < 4; ++k) a[k] += (double)S.red[i][k];
+        const float t = S.red[i][4];
+        mm = (t > mm || t != t) ? t : mm;
+      }
+      atomicAdd(&A.stats->mass_dev, a[0]);
+      atomicAdd(&A.stats->mom[0], a[1]);
+      atomicAdd(&A.stats->mom[1], a[2]);
+      atomicAdd(&A.stats->mom[2], a[3]);
+      atomicMax(&A.stats->max_u2_bits, __float_as_uint(mm));
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ host launcher
+#ifndef HLBM_Q16_STAGES
+#define HLBM_Q16_STAGES 3
+#endif
+#ifndef HLBM_Q16_NB
+#define HLBM_Q16_NB 1   // measured: a second exchange buffer buys nothing (2.23 vs 2.25 ms, 512^3)
+#endif
+#ifndef HLBM_F32_STAGES
+#define HLBM_F32_STAGES 3
+#endif
+#ifndef HLBM_F32_NB
+#define HLBM_F32_NB 1   // fp32 tiles leave room for one exchange buffer next to 3 stages
+#endif
+template <bool Q16> struct InteriorCfg {
+  static constexpr int STAGES = Q16 ? HLBM_Q16_STAGES : HLBM_F32_STAGES;
+  static constexpr int NB = Q16 ? HLBM_Q16_NB : HLBM_F32_NB;
+};
+
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE>
+static cudaError_t launch_interior_t(const StepArgs& A, int nblocks, cudaStream_t st) {
+  constexpr int STAGES = InteriorCfg<Q16>::STAGES, NB = InteriorCfg<Q16>::NB;
+  constexpr int NC = Q16 ? 5 : 10;
+  const size_t smem = sizeof(Smem<NC, STAGES, NB>);
+  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STATS, QMODE, STAGES, NB>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<nblocks, kNW * 32, smem, st>>>(A);
+  return cudaGetLastError();
+}
+
+// 16-bit dispatch units (one translation unit per codec mode, hlbm_interior_q{0,1,2}.cu)
+#define HLBM_INTERIOR_Q16_UNIT(M)                                                                        \
+  cudaError_t launch_interior_q16_m##M(const StepArgs& A, int nblocks, bool force, bool special, bool dither, \
+                                       cudaStream_t st) {                                                \
+    const bool stats = A.do_stats != 0;                                                                  \
+    if (!stats) {                                                                                        \
+      if (force) return dither ? launch_interior_t<true, true, false, true, false, M>(A, nblocks, st)    \
+                               : launch_interior_t<true, true, false, false, false, M>(A, nblocks, st);  \
+      return dither ? launch_interior_t<true, false, false, true, false, M>(A, nblocks, st)              \
+                    : launch_interior_t<true, false, false, false, false, M>(A, nblocks, st);            \
+    }                                                                                                    \
+    if (special) {                                                                                       \
+      if (force) return dither ? launch_interior_t<true, true, true, true, true, M>(A, nblocks, st)      \
+                               : launch_interior_t<true, true, true, false, true, M>(A, nblocks, st);    \
+      return dither ? launch_interior_t<true, false, true, true, true, M>(A, nblocks, st)                \
+                    : launch_interior_t<true, false, true, false, true, M>(A, nblocks, st);              \
+    }                                                                                                    \
+    if (force) return dither ? launch_interior_t<true, true, false, true, true, M>(A, nblocks, st)       \
+                             : launch_interior_t<true, true, false, false, true, M>(A, nblocks, st);     \
+    return dither ? launch_interior_t<true, false, false, true, true, M>(A, nblocks, st)                 \
+                  : launch_interior_t<true, false, false, false, true, M>(A, nblocks, st);               \
+  }
+
+cudaError_t launch_interior_q16_m0(const StepArgs& A, int nblocks, bool force, bool special, bool dither,
+                                   cudaStream_t st);
+cudaError_t launch_interior_q16_m1(const StepArgs& A, int nblocks, bool force, bool special, bool dither,
+                                   cudaStream_t st);
+cudaError_t launch_interior_q16_m2(const StepArgs& A, int nblocks, bool force, bool special, bool dither,
+                                   cudaStream_t st);
+
+}  // namespace hlbm

@@ -1,0 +1,6 @@
+// 16-bit variants of fluid_interior, codec mode 2 (hlbm_launch.h: qmode).
+#include "hlbm_interior.cuh"
+
+namespace hlbm {
+HLBM_INTERIOR_Q16_UNIT(2)
+}  // namespace hlbm

@@ -3,10 +3,11 @@
 // Layout: one allocation per buffer, x-plane major so that an x-plane
 // holding every component is contiguous (halo planes ship without packing):
 //     state[xs][c][ys][zs],  xs = 0 .. nx+1 (0, nx+1: ghost planes)
-//                            ys = y + 1 in 0 .. ny+1, zs = z + 1 in 0 .. nz+1 (row stride zp)
+//                            ys = y + 1 in 0 .. ny+1, zs = z + 2 in 1 .. nz+2 (row stride zp)
 // The y/z ghost rows/columns hold the periodic images of the opposite edge; every kernel that
 // writes an edge cell also writes its images, so a tile never wraps and one TMA box per plane
-// covers it.
+// covers it.  Column 0 is padding: with z = 0 at the even column 2, every even-z cell pair is
+// an aligned 8-byte word pair (one st.global.v2 per component in the interior kernel).
 //   fp32: c = 0..9  -> d = rho-1, j_x, j_y, j_z, sneq_xx, xy, xz, yy, yz, zz   (float)
 //   q16 : c = 0..4  -> u32 words, word k = code(2k) | code(2k+1) << 16
 #pragma once
@@ -16,15 +17,17 @@
 
 namespace hlbm {
 
-constexpr int kNW = 16;          // warps per CTA = y rows held by a CTA (14 interior + 2 halo)
-constexpr int kRows = kNW - 2;   // interior rows per CTA
+constexpr int kNW = 16;          // warps per CTA = interior y rows of a tile (one row per warp)
+constexpr int kRows = kNW;       // interior rows per tile
+constexpr int kBoxRows = kNW + 2;   // rows of a plane tile in shared memory (+1 halo row per side)
 constexpr int kZW = 64;          // z cells covered by one warp (32 lanes x 2 cells)
-constexpr int kZT = 60;          // interior z cells per tile (window start 60k: 16 B-aligned TMA origin)
+constexpr int kZT = 60;          // interior z cells per tile (lanes 1..30; lanes 0 and 31 are halo)
+constexpr int kZOff = 2;         // storage column of z = 0
 constexpr int kNSlot = 18;       // exchanged values per cell pair: (cx 3) x (cy +-1) x (kz 3)
 
 struct Geo {
   int nx, ny, nz;          // local interior dims (x = slab axis)
-  int zp;                  // padded row length (>= nz + 2, multiple of 4)
+  int zp;                  // padded row length (>= nz + 3, multiple of 4)
   int64_t cstride;         // (ny+2)*zp        elements between components
   int64_t pstride;         // NC*(ny+2)*zp     elements between x planes
   int x_lo_src, x_hi_src;  // storage plane read for source plane -1 / nx ; -1 => inflow constants
@@ -62,7 +65,7 @@ struct StepArgs {
 
 // element offset of cell (y, z) of storage plane sp (component 0)
 __host__ __device__ __forceinline__ int64_t cell_off(const Geo& g, int sp, int y, int z) {
-  return (int64_t)sp * g.pstride + (int64_t)(y + 1) * g.zp + (z + 1);
+  return (int64_t)sp * g.pstride + (int64_t)(y + 1) * g.zp + (z + kZOff);
 }
 
 __host__ __device__ __forceinline__ int wrapi(int a, int n) {
