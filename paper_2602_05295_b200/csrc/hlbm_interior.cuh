@@ -7,10 +7,11 @@
 // (moments.py:25-39) -> neq split (moments.py:93-96) -> store (fp32 or 16-bit codes).
 //
 // Mapping:
-//   * tile = 16 y rows x 60 z cells, marched along x over a segment.  CTA = 16 warps; warp w
-//     owns interior row y0 + w, so every warp stores.  The rows y0-1 and y0+16 outside the
-//     tile only feed populations into it: warps 0 and 15 evaluate just those 9 populations
-//     (cy = +1 resp. -1) of their halo row per plane, a third of a row's reconstruction.
+//   * tile = 15 y rows x 60 z cells, marched along x over a segment.  CTA = 16 warps: warps
+//     1..15 own the interior rows y0 .. y0+14; warp 0 is the halo warp: per plane it evaluates
+//     only the 9 populations that enter the tile from each of the rows y0-1 (cy = +1) and
+//     y0+15 (cy = -1) -- 0.8 of a row's work, so the SMSP holding it is not the slowest one
+//     (two halo tasks on row warps would add 0.4 of a row to two SMSPs and gate every warp).
 //   * lane l holds the z pair at storage columns (zs0 + 2l, zs0 + 2l + 1); every arithmetic op
 //     is packed f32x2 (FFMA2/FADD2/FMUL2).  Lanes 1..30 are written (aligned 8-byte pairs:
 //     z = 0 sits at the even storage column kZOff); lanes 0 and 31 are the z halo.
@@ -19,11 +20,12 @@
 //   * streaming is sum-factorised by axis: z shifts are warp shuffles, y shifts exchange 18
 //     f32x2 per lane through shared memory (neighbour-only mbarrier handshakes, no CTA
 //     barrier), x shifts are the marching accumulators.
-//   * each input plane tile (64 z x 18 y x NC components) is ONE 4-D tensor TMA copy
+//   * each input plane tile (64 z x 17 y x NC components) is ONE 4-D tensor TMA copy
 //     (cp.async.bulk.tensor + mbarrier) into shared memory, STAGES planes ahead; the y/z ghost
 //     layers of the layout make every tile in-bounds (no wrap).
 #pragma once
 #include "hlbm_params.cuh"
+
 
 namespace hlbm {
 
@@ -66,8 +68,7 @@ __device__ __forceinline__ constexpr int slot_of(int cx, int cy, int kz) {
 template <int NC, int STAGES, int NB>
 struct Smem {
   uint32_t stage[STAGES][NC][kBoxRows][kZW];
-  V exch[NB][kNSlot][kNW][32];  // y exchange (NB buffers)
-  V halo[2][9][32];             // halo-row populations: [0] row y0-1 (cy=+1), [1] row y0+16 (cy=-1)
+  V exch[NB][kNSlot][kNW][32];  // y exchange (NB buffers); "row" 0 = halo warp (see ystage)
   uint64_t bar[STAGES];         // TMA stage full (1 arrival + tx bytes)
   uint64_t full[NB][kNW];       // warp w's exchange slots of buffer b written (1 arrival)
   uint64_t empty[NB][kNW];      // ... consumed by every y-stage neighbour of w
@@ -172,33 +173,32 @@ __device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], 
   zlevel<0>(G, gz[0], gz[1], gz[2]);
 }
 
-// halo row: only the populations that enter the tile (cy = CY), for every cx
+// halo row: only the populations that enter the tile (cy = CY), for every cx, into the
+// exchange slots of "row" 0 (cy = +1 slots: row y0-1; cy = -1 slots: row y0+15)
 template <int CY>
-__device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*hs)[32], int lane) {
+__device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32], int lane) {
   V a, b, c;
-  { const GLev G = glevel<-1>(C); zlevel<CY>(G, a, b, c); hs[0][lane] = a; hs[1][lane] = b; hs[2][lane] = c; }
-  { const GLev G = glevel<0>(C);  zlevel<CY>(G, a, b, c); hs[3][lane] = a; hs[4][lane] = b; hs[5][lane] = c; }
-  { const GLev G = glevel<1>(C);  zlevel<CY>(G, a, b, c); hs[6][lane] = a; hs[7][lane] = b; hs[8][lane] = c; }
+  { const GLev G = glevel<-1>(C); zlevel<CY>(G, a, b, c);
+    exch[slot_of(-1, CY, 0)][0][lane] = a; exch[slot_of(-1, CY, 1)][0][lane] = b; exch[slot_of(-1, CY, 2)][0][lane] = c; }
+  { const GLev G = glevel<0>(C); zlevel<CY>(G, a, b, c);
+    exch[slot_of(0, CY, 0)][0][lane] = a; exch[slot_of(0, CY, 1)][0][lane] = b; exch[slot_of(0, CY, 2)][0][lane] = c; }
+  { const GLev G = glevel<1>(C); zlevel<CY>(G, a, b, c);
+    exch[slot_of(1, CY, 0)][0][lane] = a; exch[slot_of(1, CY, 1)][0][lane] = b; exch[slot_of(1, CY, 2)][0][lane] = c; }
 }
 
 // y-stage for one cx: neighbour contributions (row y-1 sent cy=+1, row y+1 sent cy=-1)
-// as t = A + B (even in cy) and d = A - B (odd in cy), per kz.
+// as t = A + B (even in cy) and d = A - B (odd in cy), per kz.  The exchange rows form a ring
+// over the warps: row warp w (1..15) reads cy=+1 slots of w-1 and cy=-1 slots of (w+1) mod 16,
+// so the first row reads the halo warp's row-(y0-1) values and the last its row-(y0+15) values.
 template <int CX>
-__device__ __forceinline__ void ystage(V (*exch)[kNW][32], const V (*halo)[9][32], int w, int lane, V t[3],
-                                       V d[2]) {
-  V A0, A1, A2, B0, B1, B2;
-  if (w == 0) {
-    A0 = halo[0][(CX + 1) * 3 + 0][lane]; A1 = halo[0][(CX + 1) * 3 + 1][lane]; A2 = halo[0][(CX + 1) * 3 + 2][lane];
-  } else {
-    A0 = exch[slot_of(CX, 1, 0)][w - 1][lane]; A1 = exch[slot_of(CX, 1, 1)][w - 1][lane];
-    A2 = exch[slot_of(CX, 1, 2)][w - 1][lane];
-  }
-  if (w == kNW - 1) {
-    B0 = halo[1][(CX + 1) * 3 + 0][lane]; B1 = halo[1][(CX + 1) * 3 + 1][lane]; B2 = halo[1][(CX + 1) * 3 + 2][lane];
-  } else {
-    B0 = exch[slot_of(CX, -1, 0)][w + 1][lane]; B1 = exch[slot_of(CX, -1, 1)][w + 1][lane];
-    B2 = exch[slot_of(CX, -1, 2)][w + 1][lane];
-  }
+__device__ __forceinline__ void ystage(V (*exch)[kNW][32], int w, int lane, V t[3], V d[2]) {
+  const int wu = w - 1, wd = (w + 1) & (kNW - 1);
+  const V A0 = exch[slot_of(CX, 1, 0)][wu][lane];
+  const V A1 = exch[slot_of(CX, 1, 1)][wu][lane];
+  const V A2 = exch[slot_of(CX, 1, 2)][wu][lane];
+  const V B0 = exch[slot_of(CX, -1, 0)][wd][lane];
+  const V B1 = exch[slot_of(CX, -1, 1)][wd][lane];
+  const V B2 = exch[slot_of(CX, -1, 2)][wd][lane];
   t[0] = vadd(A0, B0); t[1] = vadd(A1, B1); t[2] = vadd(A2, B2);
   d[0] = vsub(A0, B0); d[1] = vsub(A1, B1);
 }
@@ -383,9 +383,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
   const int xsi = item / g.nyt;
   const int zs0 = zt * kZT;                 // storage column of the window start
   const int y0 = yt * kRows;                // first interior row; the box starts at storage row y0
-  const int yrow = y0 + w;                  // logical y of this warp's row
+  const int yrow = y0 + w - 1;              // logical y of this warp's row (row warps 1..15)
   const int zc = zs0 - kZOff + 2 * lane;    // logical z of this lane's .x cell (even)
-  const bool wr = (yrow < g.ny) && (lane >= 1) && (lane <= 30) && (zc < g.nz);
+  const bool wr = (w >= 1) && (yrow < g.ny) && (lane >= 1) && (lane <= 30) && (zc < g.nz);
   const int xs = xsi * g.xseg, xe = min(xs + g.xseg, g.nx);
   const int NP = xe - xs + 2;
   const bool lo_inflow = g.x_lo_src < 0, hi_inflow = g.x_hi_src < 0;
@@ -396,11 +396,12 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       mbar_init(&S.bar[s], 1);
       S.stage_cnt[s] = 0;
     }
-    // warp v's slots are read by its neighbours v-1 and v+1 inside the tile
+    // readers of exchange row v: cy=+1 slots by v+1 (row warps), cy=-1 slots by v-1 (row warps)
+    // or, for the halo row 0, by the last row warp
     for (int b = 0; b < NB; ++b)
       for (int v = 0; v < kNW; ++v) {
         mbar_init(&S.full[b][v], 1);
-        mbar_init(&S.empty[b][v], (v > 0) + (v < kNW - 1));
+        mbar_init(&S.empty[b][v], v == 0 ? 2 : (v + 1 <= kNW - 1) + (v - 1 >= 1));
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
@@ -411,118 +412,142 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       issue_plane<NC>(A, xs - 1 + it, S.stage[it], &S.bar[it], zs0, y0);
   }
 
-  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-  Part9 Ac, Ad;   // dest p-1 partials (two register sets: the loop is unrolled x2)
-  Part6 Bc, Bd;   // dest p partials
-#pragma unroll
-  for (int k = 0; k < 6; ++k) Ac.a[k] = Bc.a[k] = vsplat(0.f);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
   int st = 0;
   uint32_t sph = 0;
-
-  // one source plane: (A9, B6) carried in, (nb, nn) carried out
-  auto body = [&](const int it, const Part9& A9, const Part6& B6, Part9& nb, Part6& nn) {
-    const int p = xs - 1 + it;
-    const int q = p - 1;   // destination plane finished in this iteration
-    const bool store_plane = wr && it >= 2;
-    const int b = (NB == 2) ? (it & 1) : 0;
-    const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
-    V (*exch)[kNW][32] = S.exch[b];
-    const bool inflow = (p < 0 && lo_inflow) || (p >= g.nx && hi_inflow);
-    mbar_wait(&S.bar[st], sph);
-    // halo rows: the 9 populations of row y0-1 (cy = +1) / y0+16 (cy = -1) entering the tile
-    if (w == 0 || w == kNW - 1) {
-      V s[10];
-      load_state<Q16, QMODE>(S.stage[st], w == 0 ? 0 : kBoxRows - 1, lane, inflow, A, s);
-      const Coef<V> C =
-          coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-      if (w == 0) recon_halo<1>(C, S.halo[0], lane);
-      else recon_halo<-1>(C, S.halo[1], lane);
-    }
-    V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
-    {
-      V s[10];
-      load_state<Q16, QMODE>(S.stage[st], w + 1, lane, inflow, A, s);
-      const Coef<V> C =
-          coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-      // the stage has been consumed by this warp (C depends on every loaded value); the last
-      // warp to get here refills it with the plane STAGES iterations ahead
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t old = atomicAdd(&S.stage_cnt[st], 1u);
-        if (old == kNW - 1) {
-          S.stage_cnt[st] = 0;
-          if (it + STAGES < NP) issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, y0);
-        }
-      }
-      // my slots of buffer b were read by my neighbours NB planes ago
-      mbar_wait(&S.empty[b][w], eph ^ 1u);
-      V gz[3];
-      // cx = -1 -> dest q (final contribution)
-      const V c4 = vsplat(4.0f), cm4 = vsplat(-4.0f), c16 = vsplat(16.0f);
-      recon_row<-1>(C, exch, w, lane, gz);          // gz at 1/4 scale (cy = 0)
-      fin[0] = vfma(gz[0], c4, A9.a[0]);
-      fin[3] = vfma(gz[1], c4, A9.a[1]);
-      fin[9] = vfma(gz[2], c4, A9.a[2]);
-      fin[2] = A9.a[3];
-      fin[8] = A9.a[4];
-      fin[7] = A9.a[5];
-      fin[1] = vfma(gz[0], cm4, A9.b[0]);
-      fin[6] = vfma(gz[1], cm4, A9.b[1]);
-      fin[5] = A9.b[2];
-      fin[4] = vfma(gz[0], c4, A9.b[0]);
-      // cx = 0 -> dest p                          (gz at 1/16 scale: cx = 0 and cy = 0)
-      recon_row<0>(C, exch, w, lane, gz);
-      nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
-      nb.a[0] = vfma(gz[0], c16, B6.a[0]);
-      nb.a[1] = vfma(gz[1], c16, B6.a[1]);
-      nb.a[2] = vfma(gz[2], c16, B6.a[2]);
-      nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
-      // cx = +1 -> dest p+1                       (gz at 1/4 scale, folded after the y-stage)
-      recon_row<1>(C, exch, w, lane, gz);
-      nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
-    }
-    if (++st == STAGES) { st = 0; sph ^= 1u; }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.full[b][w]);
-    if (w > 0) mbar_wait(&S.full[b][w - 1], eph);
-    if (w < kNW - 1) mbar_wait(&S.full[b][w + 1], eph);
-    {
-      V t[3], d[2];
-      ystage<-1>(exch, S.halo, w, lane, t, d);
-      fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
-      fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
-      fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
-      fin[4] = vadd(fin[4], t[0]);
-      ystage<0>(exch, S.halo, w, lane, t, d);       // cx = 0 slots are at 1/4 scale
-      const V c4 = vsplat(4.0f);
-      nb.a[0] = vfma(t[0], c4, nb.a[0]); nb.a[1] = vfma(t[1], c4, nb.a[1]); nb.a[2] = vfma(t[2], c4, nb.a[2]);
-      nb.a[3] = vfma(d[0], c4, nb.a[3]); nb.a[4] = vfma(d[1], c4, nb.a[4]); nb.a[5] = vfma(t[0], c4, nb.a[5]);
-      ystage<1>(exch, S.halo, w, lane, t, d);
-      nn.a[0] = vfma(nn.a[0], c4, t[0]); nn.a[1] = vfma(nn.a[1], c4, t[1]); nn.a[2] = vfma(nn.a[2], c4, t[2]);
-      nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
-    }
+  // this warp is done reading stage st; the last warp to get here refills it with the plane
+  // STAGES iterations ahead
+  auto consumed = [&](const int it) {
     __syncwarp();
     if (lane == 0) {
-      if (w > 0) mbar_arrive(&S.empty[b][w - 1]);
-      if (w < kNW - 1) mbar_arrive(&S.empty[b][w + 1]);
-    }
-    if (store_plane) {
-      bool sx = STATS, sy = STATS;
-      if (STATS && SPECIAL) {   // boundary / solid cells are finished by the compacted kernels
-        const uint32_t wv =
-            __ldg(A.special_bits + ((int64_t)q * g.ny + yrow) * A.bits_row_words + (zc >> 5));
-        sx = !((wv >> (zc & 31)) & 1u);
-        sy = !((wv >> ((zc & 31) + 1)) & 1u);
+      const uint32_t old = atomicAdd(&S.stage_cnt[st], 1u);
+      if (old == kNW - 1) {
+        S.stage_cnt[st] = 0;
+        if (it + STAGES < NP) issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, y0);
       }
-      store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, sx, sy, red);
     }
   };
+  auto plane_inflow = [&](const int p) { return (p < 0 && lo_inflow) || (p >= g.nx && hi_inflow); };
 
-  for (int it = 0; it < NP; it += 2) {
-    body(it, Ac, Bc, Ad, Bd);
-    if (it + 1 < NP) body(it + 1, Ad, Bd, Ac, Bc);
+  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  if (w == 0) {
+    // ---- halo warp: the populations entering the tile from rows y0-1 and y0+15
+    for (int it = 0; it < NP; ++it) {
+      const int b = (NB == 2) ? (it & 1) : 0;
+      const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
+      const bool inflow = plane_inflow(xs - 1 + it);
+      mbar_wait(&S.bar[st], sph);
+      mbar_wait(&S.empty[b][0], eph ^ 1u);
+      {
+        V s[10];
+        load_state<Q16, QMODE>(S.stage[st], 0, lane, inflow, A, s);
+        const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+        recon_halo<1>(C, S.exch[b], lane);
+      }
+      {
+        V s[10];
+        load_state<Q16, QMODE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
+        const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+        consumed(it);
+        recon_halo<-1>(C, S.exch[b], lane);
+      }
+      if (++st == STAGES) { st = 0; sph ^= 1u; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.full[b][0]);
+    }
+  } else {
+    // ---- row warps
+    Part9 Ac, Ad;   // dest p-1 partials (two register sets: the loop is unrolled x2)
+    Part6 Bc, Bd;   // dest p partials
+#pragma unroll
+    for (int k = 0; k < 6; ++k) Ac.a[k] = Bc.a[k] = vsplat(0.f);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
+    const int wu = w - 1, wd = (w + 1) & (kNW - 1);   // exchange rows read by this warp
+
+    // one source plane: (A9, B6) carried in, (nb, nn) carried out
+    auto body = [&](const int it, const Part9& A9, const Part6& B6, Part9& nb, Part6& nn) {
+      const int p = xs - 1 + it;
+      const int q = p - 1;   // destination plane finished in this iteration
+      const bool store_plane = wr && it >= 2;
+      const int b = (NB == 2) ? (it & 1) : 0;
+      const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
+      V (*exch)[kNW][32] = S.exch[b];
+      mbar_wait(&S.bar[st], sph);
+      V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
+      {
+        V s[10];
+        load_state<Q16, QMODE>(S.stage[st], w, lane, plane_inflow(p), A, s);
+        const Coef<V> C =
+            coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+        consumed(it);   // C depends on every loaded value
+        // my slots of buffer b were read by my neighbours NB planes ago
+        mbar_wait(&S.empty[b][w], eph ^ 1u);
+        V gz[3];
+        // cx = -1 -> dest q (final contribution)
+        const V c4 = vsplat(4.0f), cm4 = vsplat(-4.0f), c16 = vsplat(16.0f);
+        recon_row<-1>(C, exch, w, lane, gz);          // gz at 1/4 scale (cy = 0)
+        fin[0] = vfma(gz[0], c4, A9.a[0]);
+        fin[3] = vfma(gz[1], c4, A9.a[1]);
+        fin[9] = vfma(gz[2], c4, A9.a[2]);
+        fin[2] = A9.a[3];
+        fin[8] = A9.a[4];
+        fin[7] = A9.a[5];
+        fin[1] = vfma(gz[0], cm4, A9.b[0]);
+        fin[6] = vfma(gz[1], cm4, A9.b[1]);
+        fin[5] = A9.b[2];
+        fin[4] = vfma(gz[0], c4, A9.b[0]);
+        // cx = 0 -> dest p                          (gz at 1/16 scale: cx = 0 and cy = 0)
+        recon_row<0>(C, exch, w, lane, gz);
+        nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
+        nb.a[0] = vfma(gz[0], c16, B6.a[0]);
+        nb.a[1] = vfma(gz[1], c16, B6.a[1]);
+        nb.a[2] = vfma(gz[2], c16, B6.a[2]);
+        nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
+        // cx = +1 -> dest p+1                       (gz at 1/4 scale, folded after the y-stage)
+        recon_row<1>(C, exch, w, lane, gz);
+        nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
+      }
+      if (++st == STAGES) { st = 0; sph ^= 1u; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.full[b][w]);
+      mbar_wait(&S.full[b][wu], eph);
+      mbar_wait(&S.full[b][wd], eph);
+      {
+        V t[3], d[2];
+        ystage<-1>(exch, w, lane, t, d);
+        fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
+        fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
+        fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
+        fin[4] = vadd(fin[4], t[0]);
+        ystage<0>(exch, w, lane, t, d);       // cx = 0 slots are at 1/4 scale
+        const V c4 = vsplat(4.0f);
+        nb.a[0] = vfma(t[0], c4, nb.a[0]); nb.a[1] = vfma(t[1], c4, nb.a[1]); nb.a[2] = vfma(t[2], c4, nb.a[2]);
+        nb.a[3] = vfma(d[0], c4, nb.a[3]); nb.a[4] = vfma(d[1], c4, nb.a[4]); nb.a[5] = vfma(t[0], c4, nb.a[5]);
+        ystage<1>(exch, w, lane, t, d);
+        nn.a[0] = vfma(nn.a[0], c4, t[0]); nn.a[1] = vfma(nn.a[1], c4, t[1]); nn.a[2] = vfma(nn.a[2], c4, t[2]);
+        nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&S.empty[b][wu]);
+        mbar_arrive(&S.empty[b][wd]);
+      }
+      if (store_plane) {
+        bool sx = STATS, sy = STATS;
+        if (STATS && SPECIAL) {   // boundary / solid cells are finished by the compacted kernels
+          const uint32_t wv =
+              __ldg(A.special_bits + ((int64_t)q * g.ny + yrow) * A.bits_row_words + (zc >> 5));
+          sx = !((wv >> (zc & 31)) & 1u);
+          sy = !((wv >> ((zc & 31) + 1)) & 1u);
+        }
+        store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, sx, sy, red);
+      }
+    };
+
+    for (int it = 0; it < NP; it += 2) {
+      body(it, Ac, Bc, Ad, Bd);
+      if (it + 1 < NP) body(it + 1, Ad, Bd, Ac, Bc);
+    }
   }
 
   if (STATS) {

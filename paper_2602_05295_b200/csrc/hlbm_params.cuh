@@ -17,9 +17,9 @@
 
 namespace hlbm {
 
-constexpr int kNW = 16;          // warps per CTA = interior y rows of a tile (one row per warp)
-constexpr int kRows = kNW;       // interior rows per tile
-constexpr int kBoxRows = kNW + 2;   // rows of a plane tile in shared memory (+1 halo row per side)
+constexpr int kNW = 16;          // warps per CTA: 1 halo warp + one warp per interior y row
+constexpr int kRows = kNW - 1;   // interior rows per tile
+constexpr int kBoxRows = kRows + 2;   // rows of a plane tile in shared memory (+1 halo row per side)
 constexpr int kZW = 64;          // z cells covered by one warp (32 lanes x 2 cells)
 constexpr int kZT = 60;          // interior z cells per tile (lanes 1..30; lanes 0 and 31 are halo)
 constexpr int kZOff = 2;         // storage column of z = 0
