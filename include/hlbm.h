@@ -134,6 +134,17 @@ int hlbm_set_step_count(hlbm_ctx* ctx, int64_t step);
 int hlbm_set_stream(hlbm_ctx* ctx, void* cuda_stream);
 int hlbm_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
                      int64_t* bytes);
+/* the same planes of the NEXT state buffer (the one the step in progress writes): the overlapped
+ * schedule sends a step's edge planes while the bulk of that step is still being computed */
+int hlbm_next_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                          int64_t* bytes);
+/* one step split into x-ranges (edge planes first, bulk later): step_begin resets
+ * the statistics when with_stats, step_range enqueues the interior + boundary kernels for the
+ * destination planes [x_begin, x_end) of the slab, step_end makes the written buffer current.
+ * Ranges of one step must be disjoint; their union must be [0, nx). */
+int hlbm_step_begin(hlbm_ctx* ctx, int32_t with_stats);
+int hlbm_step_range(hlbm_ctx* ctx, int32_t x_begin, int32_t x_end);
+int hlbm_step_end(hlbm_ctx* ctx);
 /* device pointer of the current state buffer and its size (bytes) */
 int hlbm_state_buffer(hlbm_ctx* ctx, void** ptr, int64_t* bytes);
 int64_t hlbm_step_count(const hlbm_ctx* ctx);

@@ -75,6 +75,11 @@ SIGNATURES = {
     "hlbm_set_stream": (C.c_int, [_P, _P]),
     "hlbm_halo_planes": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                                    C.POINTER(C.c_int64)]),
+    "hlbm_next_halo_planes": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                                        C.POINTER(C.c_int64)]),
+    "hlbm_step_begin": (C.c_int, [_P, C.c_int32]),
+    "hlbm_step_range": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "hlbm_step_end": (C.c_int, [_P]),
     "hlbm_state_buffer": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64)]),
     "hlbm_step_count": (C.c_int64, [_P]),
     "hlbm_launch_count": (C.c_int64, [_P]),

@@ -46,6 +46,8 @@ struct hlbm_ctx {
   int bits_row_words = 0;
   MeshLinks mesh;                // triangle-mesh cut links (replaces the voxel lists when set)
   float solid_v[3] = {0, 0, 0}, solid_w[3] = {0, 0, 0}, solid_c[3] = {0, 0, 0};
+  std::vector<int64_t> off_b, off_s, off_m;   // per-plane offsets (nx+1) into the sorted lists
+  int pending_stats = 0;                      // statistics requested for the step in progress
   int64_t steps = 0;
   int64_t launches = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -86,8 +88,9 @@ int auto_xseg(int nx, int tiles_yz, int sms) {
   return best;
 }
 
-Geo make_geo(const hlbm_ctx* ctx) {
+Geo make_geo(const hlbm_ctx* ctx, int xb = 0, int xr = -1) {
   const hlbm_config& c = ctx->cfg;
+  if (xr < 0) xr = c.nx;
   Geo g{};
   g.nx = c.nx; g.ny = c.ny; g.nz = c.nz;
   g.zp = ctx->zp;
@@ -97,8 +100,11 @@ Geo make_geo(const hlbm_ctx* ctx) {
   g.x_hi_src = ctx->x_hi_src;
   g.nzt = (c.nz + kZT - 1) / kZT;
   g.nyt = (c.ny + kRows - 1) / kRows;
-  g.xseg = c.xseg > 0 ? std::min(c.xseg, c.nx) : auto_xseg(c.nx, g.nzt * g.nyt, ctx->num_sms);
-  g.nxs = (c.nx + g.xseg - 1) / g.xseg;
+  const int nr = std::max(xr - xb, 0);
+  g.xb = xb;
+  g.xr = xr;
+  g.xseg = c.xseg > 0 ? std::min(c.xseg, std::max(nr, 1)) : auto_xseg(std::max(nr, 1), g.nzt * g.nyt, ctx->num_sms);
+  g.nxs = nr > 0 ? (nr + g.xseg - 1) / g.xseg : 0;
   g.gx0 = c.x0; g.gny = c.gny; g.gnz = c.gnz; g.gnx_total = c.gnx;
   return g;
 }
@@ -109,12 +115,12 @@ uint32_t step_key(int64_t step, uint32_t seed) {   // oracle/codec.py: step_key
   return mix32((uint32_t)v);
 }
 
-StepArgs make_args(hlbm_ctx* ctx, int with_stats) {
+StepArgs make_args(hlbm_ctx* ctx, int with_stats, int xb = 0, int xr = -1) {
   StepArgs A{};
   A.tmap_in = ctx->tmap[ctx->cur];
   A.in = ctx->buf[ctx->cur];
   A.out = ctx->buf[1 - ctx->cur];
-  A.g = make_geo(ctx);
+  A.g = make_geo(ctx, xb, xr);
   A.R = ctx->R;
   A.Q = ctx->Q;
   for (int i = 0; i < 10; ++i) A.inflow[i] = ctx->inflow[i];
@@ -170,6 +176,57 @@ void free_mesh(hlbm_ctx* ctx) {
 
 bool has_force(const hlbm_ctx* ctx) {
   return ctx->cfg.force[0] != 0.0 || ctx->cfg.force[1] != 0.0 || ctx->cfg.force[2] != 0.0;
+}
+
+// offsets[x] = first position in the sorted local-index list whose cell lies in plane >= x
+int plane_offsets(hlbm_ctx* ctx, const int64_t* d_cells, int64_t n, std::vector<int64_t>& off) {
+  const hlbm_config& c = ctx->cfg;
+  const int64_t pl = (int64_t)c.ny * c.nz;
+  off.assign((size_t)c.nx + 1, n);
+  if (n == 0) { std::fill(off.begin(), off.end(), 0); return HLBM_OK; }
+  std::vector<int64_t> h((size_t)n);
+  CK(cudaMemcpy(h.data(), d_cells, n * 8, cudaMemcpyDeviceToHost));
+  int64_t i = 0;
+  for (int x = 0; x <= c.nx; ++x) {
+    while (i < n && h[(size_t)i] / pl < x) ++i;
+    off[(size_t)x] = i;
+  }
+  return HLBM_OK;
+}
+
+// interior kernel + compacted boundary kernels for destination planes [xb, xr)
+int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_interior = nullptr) {
+  if (xr <= xb) return HLBM_OK;
+  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
+  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
+  StepArgs A = make_args(ctx, with_stats, xb, xr);
+  CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
+  ++ctx->launches;
+  if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
+  auto sub = [&](const std::vector<int64_t>& off, int64_t n, int64_t& a, int64_t& cnt) {
+    if (off.empty()) { a = 0; cnt = (xb == 0 && xr == ctx->cfg.nx) ? n : 0; return; }
+    a = off[(size_t)xb];
+    cnt = off[(size_t)xr] - a;
+  };
+  int64_t a, cnt;
+  sub(ctx->off_b, ctx->nb, a, cnt);
+  if (cnt > 0) {
+    CK(launch_pull_cells(A, ctx->d_bcells + a, ctx->d_bmasks + a, cnt, 0, q16, force, dither, ctx->stream));
+    ++ctx->launches;
+  }
+  sub(ctx->off_s, ctx->ns, a, cnt);
+  if (cnt > 0) {
+    CK(launch_pull_cells(A, ctx->d_scells + a, nullptr, cnt, 1, q16, force, dither, ctx->stream));
+    ++ctx->launches;
+  }
+  sub(ctx->off_m, ctx->mesh.nb, a, cnt);
+  if (cnt > 0) {
+    StepArgs Am = A;
+    Am.cut_t = ctx->mesh.t32 + a * 27;
+    CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, ctx->stream));
+    ++ctx->launches;
+  }
+  return HLBM_OK;
 }
 
 }  // namespace
@@ -344,6 +401,19 @@ int hlbm_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_
                      int64_t* bytes) {
   if (!ctx) return HLBM_EINVAL;
   char* b = (char*)ctx->buf[ctx->cur];
+  const int64_t pb = ctx->plane_elems * 4;
+  if (send_lo) *send_lo = b + 1 * pb;
+  if (send_hi) *send_hi = b + (int64_t)ctx->cfg.nx * pb;
+  if (recv_lo) *recv_lo = b;
+  if (recv_hi) *recv_hi = b + (int64_t)(ctx->cfg.nx + 1) * pb;
+  if (bytes) *bytes = pb;
+  return HLBM_OK;
+}
+
+int hlbm_next_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                          int64_t* bytes) {
+  if (!ctx) return HLBM_EINVAL;
+  char* b = (char*)ctx->buf[1 - ctx->cur];
   const int64_t pb = ctx->plane_elems * 4;
   if (send_lo) *send_lo = b + 1 * pb;
   if (send_hi) *send_hi = b + (int64_t)ctx->cfg.nx * pb;
@@ -543,6 +613,9 @@ int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, c
       else { ctx->d_scells = cells; ctx->ns = tot; }
     }
   }
+  if (int r = plane_offsets(ctx, ctx->d_bcells, ctx->nb, ctx->off_b)) return r;
+  if (int r = plane_offsets(ctx, ctx->d_scells, ctx->ns, ctx->off_s)) return r;
+  ctx->off_m.clear();
   if (ctx->nb + ctx->ns > 0) {
     ctx->bits_row_words = (c.nz + 31) / 32;
     CK(cudaMalloc(&ctx->d_bits, (int64_t)c.nx * c.ny * ctx->bits_row_words * 4));
@@ -601,6 +674,9 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
     cudaFree(dV);
     cudaFree(dF);
   }
+  ctx->off_b.clear();
+  ctx->off_s.clear();
+  if (int r = plane_offsets(ctx, ctx->mesh.cells, ctx->mesh.nb, ctx->off_m)) return r;
   if (ctx->mesh.nb > 0) {
     ctx->bits_row_words = (c.nz + 31) / 32;
     const int64_t nw = (int64_t)c.nx * c.ny * ctx->bits_row_words;
@@ -644,29 +720,34 @@ int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n
 
 int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
-  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
-  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   for (int s = 0; s < nsteps; ++s) {
     const int st = (with_stats && s == nsteps - 1) ? 1 : 0;
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
-    StepArgs A = make_args(ctx, st);
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
-    ++ctx->launches;
-    if (ctx->nb) {
-      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
-      ++ctx->launches;
-    }
-    if (ctx->ns) {
-      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
-      ++ctx->launches;
-    }
-    if (ctx->mesh.nb) {
-      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream));
-      ++ctx->launches;
-    }
+    if (int r = run_range(ctx, 0, ctx->cfg.nx, st)) return r;
     ctx->cur = 1 - ctx->cur;
     ++ctx->steps;
   }
+  return HLBM_OK;
+}
+
+int hlbm_step_begin(hlbm_ctx* ctx, int32_t with_stats) {
+  if (!ctx) return HLBM_EINVAL;
+  ctx->pending_stats = with_stats ? 1 : 0;
+  if (with_stats) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+  return HLBM_OK;
+}
+
+int hlbm_step_range(hlbm_ctx* ctx, int32_t x_begin, int32_t x_end) {
+  if (!ctx) return HLBM_EINVAL;
+  if (x_begin < 0 || x_end > ctx->cfg.nx || x_begin > x_end) return fail(ctx, HLBM_EINVAL, "bad x range");
+  return run_range(ctx, x_begin, x_end, ctx->pending_stats);
+}
+
+int hlbm_step_end(hlbm_ctx* ctx) {
+  if (!ctx) return HLBM_EINVAL;
+  ctx->cur = 1 - ctx->cur;
+  ++ctx->steps;
+  ctx->pending_stats = 0;
   return HLBM_OK;
 }
 
@@ -734,29 +815,12 @@ int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     if (out) { memset(out, 0, sizeof(*out)); out->step = ctx->steps; out->finite = 1; }
     return HLBM_OK;
   }
-  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
-  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   double tf = 0, ts = 0;
   for (int s = 0; s < nsteps; ++s) {
     const int st = (s == nsteps - 1) ? 1 : 0;
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
-    StepArgs A = make_args(ctx, st);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
-    ++ctx->launches;
-    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-    if (ctx->nb) {
-      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
-      ++ctx->launches;
-    }
-    if (ctx->ns) {
-      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
-      ++ctx->launches;
-    }
-    if (ctx->mesh.nb) {
-      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream));
-      ++ctx->launches;
-    }
+    if (int r = run_range(ctx, 0, ctx->cfg.nx, st, ctx->ev[1])) return r;
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     CK(cudaEventSynchronize(ctx->ev[2]));
     float a = 0, b = 0;

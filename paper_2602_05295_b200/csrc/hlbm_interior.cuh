@@ -254,13 +254,17 @@ __device__ __forceinline__ void load_state(const uint32_t (*st)[kBoxRows][kZW], 
   }
 }
 
-// a finished cell pair (z even, z+1) of row y into plane_base (component 0 of the plane), plus
-// its periodic images in the y/z ghost layers when the pair touches an edge.  E: element type
-// of the layout (float / uint32_t), W: the pair type stored (8 bytes, aligned: z + kZOff even).
+// a finished cell pair (z even, z+1) of row y: `cell` points at component 0 of the pair in its
+// plane (8-byte aligned: z + kZOff is even); the uniform component stride is g.cstride elements.
+// Edge pairs also go to their periodic images in the y/z ghost layers (plane_base = component 0
+// of the plane).  E: element type of the layout (float / uint32_t), W: the 8-byte pair type.
 template <typename E, typename W>
-__device__ __forceinline__ void put_pair(const Geo& g, E* plane_base, int y, int z, const W* vals, int ncomp) {
-  E* p = plane_base + (int64_t)(y + 1) * g.zp + (z + kZOff);
-  for (int c = 0; c < ncomp; ++c) *reinterpret_cast<W*>(p + c * g.cstride) = vals[c];
+__device__ __forceinline__ void put_pair(const Geo& g, E* cell, E* plane_base, int y, int z, const W* vals,
+                                         int ncomp) {
+  const uint32_t cs = (uint32_t)g.cstride * (uint32_t)sizeof(E);   // < 2^32 bytes per component plane
+  char* p = reinterpret_cast<char*>(cell);
+#pragma unroll
+  for (int c = 0; c < ncomp; ++c) *reinterpret_cast<W*>(p + (size_t)(c * cs)) = vals[c];
   const bool ye = (y == 0) || (y == g.ny - 1), ze = (z == 0) || (z == g.nz - 2);
   if (ye || ze) {
     const int yi = y == 0 ? g.ny : (y == g.ny - 1 ? -1 : y);
@@ -276,15 +280,16 @@ __device__ __forceinline__ void put_pair(const Geo& g, E* plane_base, int y, int
 
 // store of one finished cell pair + fused statistics; z = logical z of the .x cell (even)
 template <bool Q16, bool DITHER, bool STATS, int QMODE>
-__device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z, bool statx,
+__device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z, int64_t cell_off0, bool statx,
                                            bool staty, float red[5]) {
   const Geo& g = A.g;
-  V s[10];
-  raw_to_state(m, s);
+  V s[10], inv;
+  raw_to_state(m, s, &inv);
   const int64_t plane_off = (int64_t)(q + 1) * g.pstride;
+  const int64_t cell_off = plane_off + cell_off0;
   constexpr bool B16 = QMODE >= 1;
   if (!Q16) {
-    put_pair(g, reinterpret_cast<float*>(A.out) + plane_off, y, z, s, 10);
+    put_pair(g, reinterpret_cast<float*>(A.out) + cell_off, reinterpret_cast<float*>(A.out) + plane_off, y, z, s, 10);
   } else {
     V nz[10];
     if (DITHER) {
@@ -324,7 +329,8 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
         wd[k].y = __byte_perm(a1, b1, 0x5410);
       }
     }
-    put_pair(g, reinterpret_cast<uint32_t*>(A.out) + plane_off, y, z, wd, 5);
+    put_pair(g, reinterpret_cast<uint32_t*>(A.out) + cell_off, reinterpret_cast<uint32_t*>(A.out) + plane_off, y,
+             z, wd, 5);
     if (STATS) {
       // saturation: |r| > 1  <=>  m outside [min, max]  (rare slow path)
       bool satx, saty;
@@ -353,17 +359,22 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     }
   }
   if (STATS) {
-    if (statx) {
-      red[0] += s[0].x; red[1] += s[1].x; red[2] += s[2].x; red[3] += s[3].x;
-      const float inv = rcp_nr(1.0f + s[0].x);
-      const float u2 = (s[1].x * s[1].x + s[2].x * s[2].x + s[3].x * s[3].x) * inv * inv;
-      red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
-    }
-    if (staty) {
-      red[0] += s[0].y; red[1] += s[1].y; red[2] += s[2].y; red[3] += s[3].y;
-      const float inv = rcp_nr(1.0f + s[0].y);
-      const float u2 = (s[1].y * s[1].y + s[2].y * s[2].y + s[3].y * s[3].y) * inv * inv;
-      red[4] = (u2 > red[4] || u2 != u2) ? u2 : red[4];
+    // mass, momentum, max |u|^2 (NaN in any cell already makes the mass sum non-finite)
+    const V ju = vmul(vfma(s[3], s[3], vfma(s[2], s[2], vmul(s[1], s[1]))), vmul(inv, inv));
+    if (statx && staty) {
+      const V a = vadd(make_float2(s[0].x, s[1].x), make_float2(s[0].y, s[1].y));
+      const V c = vadd(make_float2(s[2].x, s[3].x), make_float2(s[2].y, s[3].y));
+      red[0] += a.x; red[1] += a.y; red[2] += c.x; red[3] += c.y;
+      red[4] = fmaxf(red[4], fmaxf(ju.x, ju.y));
+    } else {
+      if (statx) {
+        red[0] += s[0].x; red[1] += s[1].x; red[2] += s[2].x; red[3] += s[3].x;
+        red[4] = fmaxf(red[4], ju.x);
+      }
+      if (staty) {
+        red[0] += s[0].y; red[1] += s[1].y; red[2] += s[2].y; red[3] += s[3].y;
+        red[4] = fmaxf(red[4], ju.y);
+      }
     }
   }
 }
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
   const int yrow = y0 + w - 1;              // logical y of this warp's row (row warps 1..15)
   const int zc = zs0 - kZOff + 2 * lane;    // logical z of this lane's .x cell (even)
   const bool wr = (w >= 1) && (yrow < g.ny) && (lane >= 1) && (lane <= 30) && (zc < g.nz);
-  const int xs = xsi * g.xseg, xe = min(xs + g.xseg, g.nx);
+  const int xs = g.xb + xsi * g.xseg, xe = min(xs + g.xseg, g.xr);
   const int NP = xe - xs + 2;
   const bool lo_inflow = g.x_lo_src < 0, hi_inflow = g.x_hi_src < 0;
 
@@ -463,6 +474,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 #pragma unroll
     for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
     const int wu = w - 1, wd = (w + 1) & (kNW - 1);   // exchange rows read by this warp
+    const int64_t cell0 = (int64_t)(yrow + 1) * g.zp + (zc + kZOff);   // pair offset inside a plane
 
     // one source plane: (A9, B6) carried in, (nb, nn) carried out
     auto body = [&](const int it, const Part9& A9, const Part6& B6, Part9& nb, Part6& nn) {
@@ -540,7 +552,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
           sx = !((wv >> (zc & 31)) & 1u);
           sy = !((wv >> ((zc & 31) + 1)) & 1u);
         }
-        store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, sx, sy, red);
+        store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, cell0, sx, sy, red);
       }
     };
 

@@ -216,10 +216,11 @@ __device__ __forceinline__ void eval_eo(const Coef<T>& C, T& E, T& O) {
 
 // raw moments (of ft) -> stored state: d = m0, j = m1, n = (Pi~ - delta d/3) - j j / rho
 template <class T>
-__device__ __forceinline__ void raw_to_state(const T m[10], T out[10]) {
+__device__ __forceinline__ void raw_to_state(const T m[10], T out[10], T* inv_out = nullptr) {
   // m: [m000, m100, m010, m001, m200, m110, m101, m020, m011, m002]
   T d = m[0];
   T inv = vrcp(vadd(d, splat<T>(1.0f)));
+  if (inv_out) *inv_out = inv;
   T d3 = vmul(d, splat<T>(1.0f / 3.0f));
   T jx = m[1], jy = m[2], jz = m[3];
   T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);

@@ -32,6 +32,7 @@ struct Geo {
   int64_t pstride;         // NC*(ny+2)*zp     elements between x planes
   int x_lo_src, x_hi_src;  // storage plane read for source plane -1 / nx ; -1 => inflow constants
   int nzt, nyt, nxs, xseg; // tiling of the interior kernel
+  int xb, xr;              // destination x-range [xb, xr) of this launch (segments start at xb)
   int gx0, gny, gnz;       // slab offset in the global grid (dither key)
   int gnx_total;           // global nx
 };

@@ -10,6 +10,13 @@ The exchange runs over ``torch.distributed`` point-to-point (NCCL over NVLink on
 box, gloo in the CPU tests).  Ranks at a non-periodic x face have no neighbour there; their
 ghost plane is resolved by the BC inside the kernels (inflow constants / outflow clamp /
 wall bounce-back).
+
+Overlap: a step computes its two edge destination planes first
+(``step_range(0, 1)``, ``step_range(nx-1, nx)``), then posts the exchange of those planes
+into the neighbours' ghost planes of the buffer being written -- on a separate CUDA stream
+that waits only for the edge kernels -- while the bulk ``step_range(1, nx-1)`` runs on the
+compute stream.  The next step's kernels wait for the exchange with a stream event, never
+on the host.
 """
 
 from __future__ import annotations
@@ -98,43 +105,106 @@ def mask_ghost_planes(global_mask: np.ndarray, plan: SlabPlan):
 class DistributedSolver:
     """One rank's slab of a global grid: a ``Solver`` plus the per-step halo exchange.
 
-    ``step(n)`` = n x (exchange halos; fluid_update_step).  All ranks must call it
-    together.  Statistics are reduced over ranks with an all-reduce."""
+    ``step(n)`` = n x (edge planes; post the exchange of the written edge planes; bulk
+    planes).  All ranks must call it together.  Statistics are reduced over ranks with an
+    all-reduce.  ``solver`` may be injected (any object with the Solver stepping/halo
+    interface: step_begin / step_range / step_end / halo_tensors or halo_planes, state_version);
+    the CPU tests drive this schedule with an oracle-backed slab over gloo."""
 
     def __init__(self, global_dims: Sequence[int], config, mask: Optional[np.ndarray] = None,
-                 rank: Optional[int] = None, world: Optional[int] = None, group=None):
+                 rank: Optional[int] = None, world: Optional[int] = None, group=None, solver=None,
+                 overlap: bool = True):
         import torch
         import torch.distributed as dist
-
-        from .solver import SimGrid, Slab, Solver
 
         self.rank = dist.get_rank() if rank is None else rank
         self.world = dist.get_world_size() if world is None else world
         self.group = group
+        self.overlap = overlap
         gnx, ny, nz = (int(d) for d in global_dims)
         x_periodic = tuple(config.bc.get("x", ("periodic", "periodic"))) == ("periodic", "periodic")
         self.plan = partition(gnx, self.world, x_periodic)[self.rank]
         p = self.plan
-        slab = Slab(x0=p.x0, gnx=gnx, lo_remote=p.lo is not None, hi_remote=p.hi is not None)
-        self.solver = Solver(SimGrid((p.nx, ny, nz)), config, slab=slab)
-        if mask is not None:
-            gl, gh = mask_ghost_planes(np.asarray(mask), p)
-            self.solver.set_mask(np.asarray(mask)[p.x0:p.x0 + p.nx], gl, gh)
-        # kernels and NCCL transfers share torch's current stream: the exchange is ordered
-        # before the step without host synchronisation
-        self.solver.set_stream(torch.cuda.current_stream().cuda_stream)
         self._torch = torch
+        self._cuda = solver is None and torch.cuda.is_available()
+        if solver is None:
+            from .solver import SimGrid, Slab, Solver
 
-    def exchange(self):
-        (send_lo, send_hi, recv_lo, recv_hi), nbytes = self.solver.halo_planes()
-        t = [device_view(ptr, nbytes) for ptr in (send_lo, send_hi, recv_lo, recv_hi)]
+            slab = Slab(x0=p.x0, gnx=gnx, lo_remote=p.lo is not None, hi_remote=p.hi is not None)
+            solver = Solver(SimGrid((p.nx, ny, nz)), config, slab=slab)
+            if mask is not None:
+                gl, gh = mask_ghost_planes(np.asarray(mask), p)
+                solver.set_mask(np.asarray(mask)[p.x0:p.x0 + p.nx], gl, gh)
+        self.solver = solver
+        self._comm_stream = None
+        self._comm_done = None
+        if self._cuda:
+            # kernels run on torch's current stream; the halo exchange on its own stream
+            self.solver.set_stream(torch.cuda.current_stream().cuda_stream)
+            self._comm_stream = torch.cuda.Stream()
+        self._synced_version = None   # solver state version whose ghost planes are exchanged
+
+    # ------------------------------------------------------------------ exchange
+    def _halo_tensors(self, next_buffer: bool):
+        if hasattr(self.solver, "halo_tensors"):
+            return self.solver.halo_tensors(next_buffer)
+        (send_lo, send_hi, recv_lo, recv_hi), nbytes = self.solver.halo_planes(next_buffer)
+        return [device_view(ptr, nbytes) for ptr in (send_lo, send_hi, recv_lo, recv_hi)]
+
+    def exchange(self, next_buffer: bool = False):
+        """Blocking (stream-ordered on CUDA) exchange of the current -- or next -- buffer's
+        edge planes into the neighbours' ghost planes."""
+        t = self._halo_tensors(next_buffer)
         exchange_halos(t[0], t[1], t[2], t[3], self.plan, self.group)
+
+    def _post_exchange_next(self):
+        """Exchange the edge planes just written to the next buffer, overlapped with the bulk."""
+        torch = self._torch
+        if not self._cuda:
+            self.exchange(next_buffer=True)
+            return
+        compute = torch.cuda.current_stream()
+        edges_done = torch.cuda.Event()
+        edges_done.record(compute)
+        with torch.cuda.stream(self._comm_stream):
+            self._comm_stream.wait_event(edges_done)
+            self.exchange(next_buffer=True)          # NCCL work ordered on the comm stream
+            self._comm_done = torch.cuda.Event()
+            self._comm_done.record(self._comm_stream)
+
+    def _wait_halos(self):
+        if self._cuda and self._comm_done is not None:
+            self._torch.cuda.current_stream().wait_event(self._comm_done)
+            self._comm_done = None
+
+    # ------------------------------------------------------------------ stepping
+    def _state_version(self):
+        return getattr(self.solver, "state_version", 0)
+
+    def _one_step(self, with_stats: bool):
+        s = self.solver
+        nx = self.plan.nx
+        if self._synced_version != self._state_version():
+            self._wait_halos()
+            self.exchange()                             # the state was set on the host: prime
+        else:
+            self._wait_halos()                          # ghosts posted during the last step
+        s.step_begin(with_stats)
+        if not self.overlap or nx <= 2:
+            s.step_range(0, nx)
+            s.step_end()
+            self._synced_version = None                 # exchange at the next step's start
+            return
+        s.step_range(0, 1)
+        s.step_range(nx - 1, nx)
+        self._post_exchange_next()
+        s.step_range(1, nx - 1)
+        s.step_end()
+        self._synced_version = self._state_version()
 
     def step(self, n: int = 1, stats: bool = True):
         for k in range(n):
-            self.exchange()
-            last = stats and k == n - 1
-            self.solver.step_async(1, with_stats=last)
+            self._one_step(stats and k == n - 1)
         if stats:
             return self.reduce_stats(self.solver.read_stats())
         return None
@@ -142,10 +212,11 @@ class DistributedSolver:
     def reduce_stats(self, st):
         import torch
         import torch.distributed as dist
+        dev = "cuda" if self._cuda else "cpu"
         v = torch.tensor([st.mass, *st.momentum, st.n_fluid, *st.saturation], dtype=torch.float64,
-                         device="cuda")
+                         device=dev)
         dist.all_reduce(v, group=self.group)
-        m = torch.tensor([st.max_u], dtype=torch.float64, device="cuda")
+        m = torch.tensor([st.max_u], dtype=torch.float64, device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
         v = v.cpu().numpy()
         st.mass = float(v[0])

@@ -139,6 +139,7 @@ class Solver:
         self.grid = grid
         self.config = config
         self.slab = slab
+        self.state_version = 0   # bumped by every host-side state change and step (halo sync)
         self._lib = _lib.load()
         nx, ny, nz = grid.dims
         c = _lib.HlbmConfig()
@@ -241,6 +242,7 @@ class Solver:
         return cells, masks, t, tri
 
     def set_moments(self, rho, mom, stress):
+        self.state_version += 1
         nx, ny, nz = self.grid.dims
         rho = np.ascontiguousarray(rho, dtype=np.float64)
         mom = np.ascontiguousarray(mom, dtype=np.float64)
@@ -259,17 +261,20 @@ class Solver:
         self.set_moments(rho, mom, st)
 
     def init_modes(self, modes: np.ndarray, rho0: float = 1.0):
+        self.state_version += 1
         modes = np.ascontiguousarray(modes, dtype=np.float64).reshape(-1, 7)
         self._chk(self._lib.hlbm_init_modes(self._ctx, float(rho0), _lib.dptr(modes), len(modes)))
 
     # ---------------------------------------------------------------- stepping
     def step(self, n: int = 1) -> StepStats:
+        self.state_version += 1
         s = _lib.HlbmStats()
         self._chk(self._lib.hlbm_step(self._ctx, int(n), C.byref(s)))
         self._last = StepStats._from_c(s)
         return self._last
 
     def step_async(self, n: int = 1, with_stats: bool = False):
+        self.state_version += 1
         self._chk(self._lib.hlbm_step_async(self._ctx, int(n), int(with_stats)))
 
     def read_stats(self) -> StepStats:
@@ -279,6 +284,7 @@ class Solver:
 
     def step_reference(self, n: int = 1):
         """Full-grid update with the per-cell pull kernel (GPU cross-check of the fast kernel)."""
+        self.state_version += 1
         self._chk(self._lib.hlbm_step_reference(self._ctx, int(n)))
 
     def set_stream(self, stream_ptr: int):
@@ -374,6 +380,7 @@ class Solver:
 
     @codes.setter
     def codes(self, words):
+        self.state_version += 1
         w = np.ascontiguousarray(words, dtype=np.uint32)
         if w.shape != (5,) + self.grid.dims:
             raise ValueError("codes must be (5, nx, ny, nz) uint32")
@@ -388,6 +395,7 @@ class Solver:
         return w
 
     def set_state(self, words, step=None):
+        self.state_version += 1
         nx, ny, nz = self.grid.dims
         q16 = self.config.precision == "q16"
         w = np.ascontiguousarray(words, dtype=np.uint32 if q16 else np.float32)
@@ -397,12 +405,25 @@ class Solver:
         if step is not None:
             self._chk(self._lib.hlbm_set_step_count(self._ctx, int(step)))
 
-    def halo_planes(self):
-        """Device pointers (send_lo, send_hi, recv_lo, recv_hi) and bytes per plane."""
+    def halo_planes(self, next_buffer: bool = False):
+        """Device pointers (send_lo, send_hi, recv_lo, recv_hi) and bytes per plane of the current
+        state buffer, or of the buffer the step in progress writes (``next_buffer``)."""
         p = [C.c_void_p() for _ in range(4)]
         nb = C.c_int64()
-        self._chk(self._lib.hlbm_halo_planes(self._ctx, *(C.byref(x) for x in p), C.byref(nb)))
+        fn = self._lib.hlbm_next_halo_planes if next_buffer else self._lib.hlbm_halo_planes
+        self._chk(fn(self._ctx, *(C.byref(x) for x in p), C.byref(nb)))
         return [x.value for x in p], nb.value
+
+    # one step split into x-ranges of destination planes (overlapped multi-GPU schedule)
+    def step_begin(self, with_stats: bool = False):
+        self._chk(self._lib.hlbm_step_begin(self._ctx, int(with_stats)))
+
+    def step_range(self, x_begin: int, x_end: int):
+        self._chk(self._lib.hlbm_step_range(self._ctx, int(x_begin), int(x_end)))
+
+    def step_end(self):
+        self.state_version += 1
+        self._chk(self._lib.hlbm_step_end(self._ctx))
 
     def state_buffer(self):
         p = C.c_void_p()
