@@ -510,30 +510,41 @@ int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmo
   return HLBM_OK;
 }
 
+// dense (NC, nx, ny, nz) host words <-> the padded device layout, one strided 3-D DMA copy per
+// component (rows of nz words; device rows at pitch zp, x-planes every NC*(ny+2) rows)
+static int copy_dense(hlbm_ctx* ctx, void* host, bool to_host) {
+  const hlbm_config& c = ctx->cfg;
+  const size_t row = (size_t)c.nz * 4;
+  for (int k = 0; k < ctx->NC; ++k) {
+    cudaMemcpy3DParms p{};
+    cudaPitchedPtr dev = make_cudaPitchedPtr(ctx->buf[ctx->cur], (size_t)ctx->zp * 4, (size_t)ctx->zp,
+                                             (size_t)ctx->NC * (c.ny + 2));
+    cudaPitchedPtr hst = make_cudaPitchedPtr((char*)host + (size_t)k * c.nx * c.ny * row, row, (size_t)c.nz,
+                                             (size_t)c.ny);
+    // device element (x+1, k, y+1, z+kZOff) in bytes/rows/slices: x-planes are the slices
+    const cudaPos dpos = make_cudaPos((size_t)kZOff * 4, (size_t)k * (c.ny + 2) + 1, 1);
+    const cudaPos hpos = make_cudaPos(0, 0, 0);
+    p.extent = make_cudaExtent(row, (size_t)c.ny, (size_t)c.nx);
+    p.kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+    if (to_host) { p.srcPtr = dev; p.srcPos = dpos; p.dstPtr = hst; p.dstPos = hpos; }
+    else { p.srcPtr = hst; p.srcPos = hpos; p.dstPtr = dev; p.dstPos = dpos; }
+    CK(cudaMemcpy3DAsync(&p, ctx->stream));
+  }
+  return HLBM_OK;
+}
+
 int hlbm_get_state(hlbm_ctx* ctx, void* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
-  const hlbm_config& c = ctx->cfg;
-  const int64_t n = (int64_t)ctx->NC * c.nx * c.ny * c.nz;
-  uint32_t* d = nullptr;
-  CK(cudaMalloc(&d, n * 4));
-  CK(launch_pack_codes(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], d, 0, ctx->stream));
-  CK(cudaMemcpyAsync(words, d, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (int r = copy_dense(ctx, words, true)) return r;
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d);
   return HLBM_OK;
 }
 
 int hlbm_set_state(hlbm_ctx* ctx, const void* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
-  const hlbm_config& c = ctx->cfg;
-  const int64_t n = (int64_t)ctx->NC * c.nx * c.ny * c.nz;
-  uint32_t* d = nullptr;
-  CK(cudaMalloc(&d, n * 4));
-  CK(cudaMemcpyAsync(d, words, n * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(launch_pack_codes(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], d, 1, ctx->stream));
+  if (int r = copy_dense(ctx, const_cast<void*>(words), false)) return r;
   CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d);
   return HLBM_OK;
 }
 
