@@ -70,10 +70,11 @@ struct Smem {
   uint32_t stage[STAGES][NC][kBoxRows][kZW];
   V exch[NB][kNSlot][kNW][32];  // y exchange (NB buffers); "row" 0 = halo warp (see ystage)
   uint64_t bar[STAGES];         // TMA stage full (1 arrival + tx bytes)
-  uint64_t full[NB][kNW];       // warp w's exchange slots of buffer b written (1 arrival)
-  uint64_t empty[NB][kNW];      // ... consumed by every y-stage neighbour of w
-  uint32_t stage_cnt[STAGES];   // warps done reading a stage; the last one refills it
+  uint64_t full[NB][kNW];       // warp w's exchange slots of buffer b written (32 lane arrivals)
+  uint64_t empty[NB][kNW];      // ... consumed by every y-stage neighbour of w (32 per reader)
+  uint64_t cons[STAGES];        // every lane of every warp has read the stage (refill allowed)
   float red[kNW][5];
+  float acc[kNW][5][32];        // per-lane statistics accumulators (STATS variants; no registers)
 };
 
 // Producer (one thread): the whole plane tile of source plane p is one tensor copy.
@@ -281,7 +282,7 @@ __device__ __forceinline__ void put_pair(const Geo& g, E* cell, E* plane_base, i
 // store of one finished cell pair + fused statistics; z = logical z of the .x cell (even)
 template <bool Q16, bool DITHER, bool STATS, int QMODE>
 __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z, int64_t cell_off0, bool statx,
-                                           bool staty, float red[5]) {
+                                           bool staty, float* acc) {
   const Geo& g = A.g;
   V s[10], inv;
   raw_to_state(m, s, &inv);
@@ -364,16 +365,16 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     if (statx && staty) {
       const V a = vadd(make_float2(s[0].x, s[1].x), make_float2(s[0].y, s[1].y));
       const V c = vadd(make_float2(s[2].x, s[3].x), make_float2(s[2].y, s[3].y));
-      red[0] += a.x; red[1] += a.y; red[2] += c.x; red[3] += c.y;
-      red[4] = fmaxf(red[4], fmaxf(ju.x, ju.y));
+      acc[0] += a.x; acc[32] += a.y; acc[64] += c.x; acc[96] += c.y;
+      acc[128] = fmaxf(acc[128], fmaxf(ju.x, ju.y));
     } else {
       if (statx) {
-        red[0] += s[0].x; red[1] += s[1].x; red[2] += s[2].x; red[3] += s[3].x;
-        red[4] = fmaxf(red[4], ju.x);
+        acc[0] += s[0].x; acc[32] += s[1].x; acc[64] += s[2].x; acc[96] += s[3].x;
+        acc[128] = fmaxf(acc[128], ju.x);
       }
       if (staty) {
-        red[0] += s[0].y; red[1] += s[1].y; red[2] += s[2].y; red[3] += s[3].y;
-        red[4] = fmaxf(red[4], ju.y);
+        acc[0] += s[0].y; acc[32] += s[1].y; acc[64] += s[2].y; acc[96] += s[3].y;
+        acc[128] = fmaxf(acc[128], ju.y);
       }
     }
   }
@@ -405,14 +406,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&S.bar[s], 1);
-      S.stage_cnt[s] = 0;
+      mbar_init(&S.cons[s], kNW * 32);
     }
     // readers of exchange row v: cy=+1 slots by v+1 (row warps), cy=-1 slots by v-1 (row warps)
     // or, for the halo row 0, by the last row warp
     for (int b = 0; b < NB; ++b)
       for (int v = 0; v < kNW; ++v) {
-        mbar_init(&S.full[b][v], 1);
-        mbar_init(&S.empty[b][v], v == 0 ? 2 : (v + 1 <= kNW - 1) + (v - 1 >= 1));
+        mbar_init(&S.full[b][v], 32);
+        mbar_init(&S.empty[b][v], 32 * (v == 0 ? 2 : (v + 1 <= kNW - 1) + (v - 1 >= 1)));
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
@@ -425,21 +426,15 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 
   int st = 0;
   uint32_t sph = 0;
-  // this warp is done reading stage st; the last warp to get here refills it with the plane
-  // STAGES iterations ahead
-  auto consumed = [&](const int it) {
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t old = atomicAdd(&S.stage_cnt[st], 1u);
-      if (old == kNW - 1) {
-        S.stage_cnt[st] = 0;
-        if (it + STAGES < NP) issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, y0);
-      }
-    }
-  };
+  // this lane is done reading stage st (the halo warp refills it once every lane has arrived)
+  auto consumed = [&]() { mbar_arrive(&S.cons[st]); };
   auto plane_inflow = [&](const int p) { return (p < 0 && lo_inflow) || (p >= g.nx && hi_inflow); };
 
-  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  float* acc = &S.acc[w][0][lane];
+  if (STATS) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc[32 * k] = 0.f;
+  }
   if (w == 0) {
     // ---- halo warp: the populations entering the tile from rows y0-1 and y0+15
     for (int it = 0; it < NP; ++it) {
@@ -458,12 +453,16 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         V s[10];
         load_state<Q16, QMODE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
         const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-        consumed(it);
+        consumed();
         recon_halo<-1>(C, S.exch[b], lane);
       }
+      mbar_arrive(&S.full[b][0]);
+      // producer: once every warp has read plane it, its stage takes plane it + STAGES
+      if (lane == 0 && it + STAGES < NP) {
+        mbar_wait(&S.cons[st], sph);
+        issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, y0);
+      }
       if (++st == STAGES) { st = 0; sph ^= 1u; }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.full[b][0]);
     }
   } else {
     // ---- row warps
@@ -491,7 +490,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         load_state<Q16, QMODE>(S.stage[st], w, lane, plane_inflow(p), A, s);
         const Coef<V> C =
             coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-        consumed(it);   // C depends on every loaded value
+        consumed();   // C depends on every loaded value
         // my slots of buffer b were read by my neighbours NB planes ago
         mbar_wait(&S.empty[b][w], eph ^ 1u);
         V gz[3];
@@ -520,8 +519,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
       }
       if (++st == STAGES) { st = 0; sph ^= 1u; }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.full[b][w]);
+      mbar_arrive(&S.full[b][w]);
       mbar_wait(&S.full[b][wu], eph);
       mbar_wait(&S.full[b][wd], eph);
       {
@@ -539,11 +537,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         nn.a[0] = vfma(nn.a[0], c4, t[0]); nn.a[1] = vfma(nn.a[1], c4, t[1]); nn.a[2] = vfma(nn.a[2], c4, t[2]);
         nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
       }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&S.empty[b][wu]);
-        mbar_arrive(&S.empty[b][wd]);
-      }
+      mbar_arrive(&S.empty[b][wu]);
+      mbar_arrive(&S.empty[b][wd]);
       if (store_plane) {
         bool sx = STATS, sy = STATS;
         if (STATS && SPECIAL) {   // boundary / solid cells are finished by the compacted kernels
@@ -552,7 +547,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
           sx = !((wv >> (zc & 31)) & 1u);
           sy = !((wv >> ((zc & 31) + 1)) & 1u);
         }
-        store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, cell0, sx, sy, red);
+        store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, cell0, sx, sy, acc);
       }
     };
 
@@ -564,6 +559,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 
   if (STATS) {
     // block reduction of the fused statistics
+    float red[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) red[k] = acc[32 * k];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float v = red[k];
