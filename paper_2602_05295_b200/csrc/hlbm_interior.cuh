@@ -61,9 +61,6 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-__device__ __forceinline__ constexpr int slot_of(int cx, int cy, int kz) {
-  return ((cx + 1) * 2 + (cy > 0 ? 0 : 1)) * 3 + kz;
-}
 
 template <int NC, int STAGES, int NB>
 struct Smem {
@@ -105,103 +102,150 @@ struct Part6 {   // only the cx=+1 contribution of source q-1: kx=1/kx=2 partial
 };
 
 // ---------------------------------------------------------------------------------------
-// Nodal evaluation of the reconstruction polynomial, by axis (weights folded as omega(0) = 4,
-// omega(+-1) = 1; centre weights are applied by the consumers' FMAs: the cx = 0 branch runs at
-// 1/4 scale and the cy = 0 results at 1/4 scale.  Scaling by a power of two commutes with
-// rounding, so the results are bit-identical to the unscaled evaluation).
-struct GLev {   // cx level: polynomial in (cy, cz) at the given cx
-  V G00, G10, G20, G01, G11, G21, G02, G12;
-};
-template <int CX>
-__device__ __forceinline__ GLev glevel(const Coef<V>& C) {
-  GLev G;
-  if (CX == 0) {   // (x 1/4)
-    G.G00 = C.K0; G.G10 = C.Ly; G.G20 = C.Qyy;
-    G.G01 = C.Lz; G.G11 = C.Qyz; G.G21 = C.Tyyz;
-    G.G02 = C.Qzz; G.G12 = C.Tyzz;
-  } else if (CX > 0) {
-    G.G00 = vadd(vadd(C.K0, C.Qxx), C.Lx); G.G10 = vadd(vadd(C.Ly, C.Txxy), C.Qxy);
-    G.G20 = vadd(C.Qyy, C.Txyy);
-    G.G01 = vadd(vadd(C.Lz, C.Txxz), C.Qxz); G.G11 = vadd(C.Qyz, C.Txyz); G.G21 = C.Tyyz;
-    G.G02 = vadd(C.Qzz, C.Txzz); G.G12 = C.Tyzz;
+// Moment-space streaming: sum factorisation by axis on the 17 monomial coefficient fields.
+// Along one axis a field F_k (monomial degree k) enters the destination's moment of order a
+// through T^{a+k} f = f(x-1) [c=+1] + (-1)^{a+k} f(x+1) [c=-1] + [a+k==0] 4 f(x)  (weights
+// w1 = omega/6 with omega(0) = 4, omega(+-1) = 1; the 1/216 is folded into the coefficients).
+// With Ap = sum_k F_k and Am = sum_k (-1)^k F_k:  out_a(x) = Ap(x-1) + (-1)^a Am(x+1)
+// + [a==0] 4 F_0(x).  z first (warp shuffles, 8 (kx,ky) groups), then y (shared-memory ring,
+// 9 (kx,az) groups), then x (register march, 6 (ay,az) groups); the truncation ax+ay+az <= 2
+// prunes the outputs after every axis.  105 packed + 32 scalar FP ops per cell pair, against
+// 127 + 36 for evaluating the 27 nodal populations first.
+
+// exchange slot of (kx, s, az): s = 0 sent to row y+1 (Yp), s = 1 sent to row y-1 (Ym)
+__device__ __forceinline__ constexpr int xslot(int kx, int s, int az) { return (kx * 2 + s) * 3 + az; }
+
+// z pull of one (kx,ky) group from its inputs F0 (kz=0), F1 (kz=1), F2 (kz=2); N inputs present
+template <int N>
+__device__ __forceinline__ void zgroup(V F0, V F1, V F2, V z[3]) {
+  V Ap, Am;
+  if (N == 3) {
+    const V P = vadd(F0, F2);
+    Ap = vadd(P, F1);
+    Am = vsub(P, F1);
+  } else if (N == 2) {
+    Ap = vadd(F0, F1);
+    Am = vsub(F0, F1);
   } else {
-    G.G00 = vsub(vadd(C.K0, C.Qxx), C.Lx); G.G10 = vsub(vadd(C.Ly, C.Txxy), C.Qxy);
-    G.G20 = vsub(C.Qyy, C.Txyy);
-    G.G01 = vsub(vadd(C.Lz, C.Txxz), C.Qxz); G.G11 = vsub(C.Qyz, C.Txyz); G.G21 = C.Tyyz;
-    G.G02 = vsub(C.Qzz, C.Txzz); G.G12 = C.Tyzz;
+    Ap = F0;
+    Am = F0;
   }
-  return G;
+  // lane pair (z0, z0+1): Ap(z-1) = (up, Ap.x), Am(z+1) = (Am.y, dn), combined with scalar adds
+  // so no shifted register pair has to be assembled
+  const float up = __shfl_up_sync(0xffffffffu, Ap.y, 1);
+  const float dn = __shfl_down_sync(0xffffffffu, Am.x, 1);
+  const V S = make_float2(__fadd_rn(up, Am.y), __fadd_rn(Ap.x, dn));
+  z[1] = make_float2(__fsub_rn(up, Am.y), __fsub_rn(Ap.x, dn));
+  z[0] = vfma(F0, vsplat(4.0f), S);
+  z[2] = S;
 }
 
-// cy level + z-stage: the z-moments (kz = 0, 1, 2) of the three populations (CX, CY, cz)
-// pulled into this lane's cells.  cz level: ft(0) = 4 B0, ft(+-1) = (B0 + B2) +- B1.
-template <int CY>
-__device__ __forceinline__ void zlevel(const GLev& G, V& g0, V& g1, V& g2) {
-  V B0, B1, B2;
-  if (CY == 0) {   // (x 1/4)
-    B0 = G.G00; B1 = G.G01; B2 = G.G02;
-  } else if (CY > 0) {
-    B0 = vadd(vadd(G.G00, G.G20), G.G10); B1 = vadd(vadd(G.G01, G.G21), G.G11); B2 = vadd(G.G02, G.G12);
+// z-stage of the groups with a given kx: Z[ky][az]
+template <int KX>
+__device__ __forceinline__ void zstage(const Coef<V>& C, V Z[3][3]) {
+  const V o = vsplat(0.f);
+  if (KX == 0) {
+    zgroup<3>(C.K0, C.Lz, C.Qzz, Z[0]);
+    zgroup<3>(C.Ly, C.Qyz, C.Tyzz, Z[1]);
+    zgroup<2>(C.Qyy, C.Tyyz, o, Z[2]);
+  } else if (KX == 1) {
+    zgroup<3>(C.Lx, C.Qxz, C.Txzz, Z[0]);
+    zgroup<2>(C.Qxy, C.Txyz, o, Z[1]);
+    zgroup<1>(C.Txyy, o, o, Z[2]);
   } else {
-    B0 = vsub(vadd(G.G00, G.G20), G.G10); B1 = vsub(vadd(G.G01, G.G21), G.G11); B2 = vsub(G.G02, G.G12);
+    zgroup<2>(C.Qxx, C.Txxz, o, Z[0]);
+    zgroup<1>(C.Txxy, o, o, Z[1]);
   }
-  const V t = vadd(B0, B2);
-  const V fp = vadd(t, B1), fm = vsub(t, B1);
-  // pull: cz=+1 comes from z-1, cz=-1 from z+1.  Lane pair (z0, z0+1):
-  //   P = (fp(z0-1), fp(z0)) = (up, fp.x),  M = (fm(z0+1), fm(z0+2)) = (fm.y, dn)
-  // formed with scalar adds so no shifted register pair has to be assembled.
-  const float up = __shfl_up_sync(0xffffffffu, fp.y, 1);
-  const float dn = __shfl_down_sync(0xffffffffu, fm.x, 1);
-  const V T2 = make_float2(__fadd_rn(up, fm.y), __fadd_rn(fp.x, dn));
-  g1 = make_float2(__fsub_rn(up, fm.y), __fsub_rn(fp.x, dn));
-  g0 = vfma(B0, vsplat(4.0f), T2);
-  g2 = T2;
 }
 
-// own row, one cx: cy = +-1 results to the exchange, cy = 0 results returned
-template <int CX>
-__device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane, V gz[3]) {
-  const GLev G = glevel<CX>(C);
-  V a, b, c;
-  zlevel<1>(G, a, b, c);
-  exch[slot_of(CX, 1, 0)][w][lane] = a;
-  exch[slot_of(CX, 1, 1)][w][lane] = b;
-  exch[slot_of(CX, 1, 2)][w][lane] = c;
-  zlevel<-1>(G, a, b, c);
-  exch[slot_of(CX, -1, 0)][w][lane] = a;
-  exch[slot_of(CX, -1, 1)][w][lane] = b;
-  exch[slot_of(CX, -1, 2)][w][lane] = c;
-  zlevel<0>(G, gz[0], gz[1], gz[2]);
+// y sums of (kx, az): Yp = sum_ky Z, Ym = sum_ky (-1)^ky Z
+template <int KX>
+__device__ __forceinline__ void ysums(const V Z[3][3], int az, V& Yp, V& Ym) {
+  if (KX < 2) {
+    const V P = vadd(Z[0][az], Z[2][az]);
+    Yp = vadd(P, Z[1][az]);
+    Ym = vsub(P, Z[1][az]);
+  } else {
+    Yp = vadd(Z[0][az], Z[1][az]);
+    Ym = vsub(Z[0][az], Z[1][az]);
+  }
 }
 
-// halo row: only the populations that enter the tile (cy = CY), for every cx, into the
-// exchange slots of "row" 0 (cy = +1 slots: row y0-1; cy = -1 slots: row y0+15)
-template <int CY>
+// own row, one kx: both y sums to the exchange, the ky = 0 centre values returned
+template <int KX>
+__device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane, V zc[3]) {
+  V Z[3][3];
+  zstage<KX>(C, Z);
+#pragma unroll
+  for (int az = 0; az < 3; ++az) {
+    V p, m;
+    ysums<KX>(Z, az, p, m);
+    exch[xslot(KX, 0, az)][w][lane] = p;
+    exch[xslot(KX, 1, az)][w][lane] = m;
+    zc[az] = Z[0][az];
+  }
+}
+
+// halo row: only the y sum that enters the tile (S = 0: row y0-1 sends Yp up; S = 1: row
+// y0+15 sends Ym down), into the exchange slots of "row" 0
+template <int S>
 __device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32], int lane) {
-  V a, b, c;
-  { const GLev G = glevel<-1>(C); zlevel<CY>(G, a, b, c);
-    exch[slot_of(-1, CY, 0)][0][lane] = a; exch[slot_of(-1, CY, 1)][0][lane] = b; exch[slot_of(-1, CY, 2)][0][lane] = c; }
-  { const GLev G = glevel<0>(C); zlevel<CY>(G, a, b, c);
-    exch[slot_of(0, CY, 0)][0][lane] = a; exch[slot_of(0, CY, 1)][0][lane] = b; exch[slot_of(0, CY, 2)][0][lane] = c; }
-  { const GLev G = glevel<1>(C); zlevel<CY>(G, a, b, c);
-    exch[slot_of(1, CY, 0)][0][lane] = a; exch[slot_of(1, CY, 1)][0][lane] = b; exch[slot_of(1, CY, 2)][0][lane] = c; }
+#define HLBM_HALO_KX(KX)                                  \
+  {                                                       \
+    V Z[3][3];                                            \
+    zstage<KX>(C, Z);                                     \
+    _Pragma("unroll") for (int az = 0; az < 3; ++az) {    \
+      V p, m;                                             \
+      ysums<KX>(Z, az, p, m);                             \
+      exch[xslot(KX, S, az)][0][lane] = S == 0 ? p : m;   \
+    }                                                     \
+  }
+  HLBM_HALO_KX(0) HLBM_HALO_KX(1) HLBM_HALO_KX(2)
+#undef HLBM_HALO_KX
 }
 
-// y-stage for one cx: neighbour contributions (row y-1 sent cy=+1, row y+1 sent cy=-1)
-// as t = A + B (even in cy) and d = A - B (odd in cy), per kz.  The exchange rows form a ring
-// over the warps: row warp w (1..15) reads cy=+1 slots of w-1 and cy=-1 slots of (w+1) mod 16,
-// so the first row reads the halo warp's row-(y0-1) values and the last its row-(y0+15) values.
-template <int CX>
-__device__ __forceinline__ void ystage(V (*exch)[kNW][32], int w, int lane, V t[3], V d[2]) {
-  const int wu = w - 1, wd = (w + 1) & (kNW - 1);
-  const V A0 = exch[slot_of(CX, 1, 0)][wu][lane];
-  const V A1 = exch[slot_of(CX, 1, 1)][wu][lane];
-  const V A2 = exch[slot_of(CX, 1, 2)][wu][lane];
-  const V B0 = exch[slot_of(CX, -1, 0)][wd][lane];
-  const V B1 = exch[slot_of(CX, -1, 1)][wd][lane];
-  const V B2 = exch[slot_of(CX, -1, 2)][wd][lane];
-  t[0] = vadd(A0, B0); t[1] = vadd(A1, B1); t[2] = vadd(A2, B2);
-  d[0] = vsub(A0, B0); d[1] = vsub(A1, B1);
+// y pull + x stage of one destination row.  The exchange rows form a ring over the warps: row
+// warp w (1..15) reads the Yp slots of wu = w-1 and the Ym slots of wd = (w+1) mod 16, so the
+// first row reads the halo warp's row-(y0-1) values and the last its row-(y0+15) values.
+//   fin (dest q):   A9 (sources q-1, q) + x-pull of Xm from this source plane (cx = -1)
+//   nb  (dest p):   B6 (source p-1) + 4 Xc (cx = 0); kx=1 partials copied
+//   nn  (dest p+1): Xp (cx = +1), identical for every ax
+// Raw-moment order of fin: m000 m100 m010 m001 m200 m110 m101 m020 m011 m002; partial index
+// order (ay,az) = 00, 01, 02, 10, 11, 20 (b: 00, 01, 10).
+__device__ __forceinline__ void yx_stage(V (*exch)[kNW][32], int wu, int wd, int lane, const V zc[3][3],
+                                         const Part9& A9, const Part6& B6, V fin[10], Part9& nb, Part6& nn) {
+  const V c4 = vsplat(4.0f);
+#pragma unroll
+  for (int az = 0; az < 3; ++az) {
+    V Y[3][3];   // [kx][ay]
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      const V A = exch[xslot(kx, 0, az)][wu][lane];
+      const V B = exch[xslot(kx, 1, az)][wd][lane];
+      const V S = vadd(A, B);
+      Y[kx][0] = vfma(zc[kx][az], c4, S);
+      if (az <= 1) Y[kx][1] = vsub(A, B);
+      if (az == 0) Y[kx][2] = S;
+    }
+#pragma unroll
+    for (int ay = 0; ay + az <= 2; ++ay) {
+      const int c = ay == 0 ? az : (ay == 1 ? 3 + az : 5);          // partial index of (ay, az)
+      const int m0 = ay == 0 ? (az == 0 ? 0 : (az == 1 ? 3 : 9)) : (ay == 1 ? (az == 0 ? 2 : 8) : 7);
+      const V P = vadd(Y[0][ay], Y[2][ay]);
+      const V Xp = vadd(P, Y[1][ay]);
+      const V Xm = vsub(P, Y[1][ay]);
+      fin[m0] = vadd(A9.a[c], Xm);
+      if (ay + az <= 1) {
+        const int bi = ay == 0 ? az : 2;                            // b index of (ay, az)
+        const int m1 = ay == 0 ? (az == 0 ? 1 : 6) : 5;
+        fin[m1] = vsub(A9.b[bi], Xm);
+        nb.b[bi] = B6.a[c];
+      }
+      if (ay + az == 0) fin[4] = vadd(A9.b[0], Xm);
+      nb.a[c] = vfma(Y[0][ay], c4, B6.a[c]);
+      nn.a[c] = Xp;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -447,14 +491,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         V s[10];
         load_state<Q16, QMODE>(S.stage[st], 0, lane, inflow, A, s);
         const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-        recon_halo<1>(C, S.exch[b], lane);
+        recon_halo<0>(C, S.exch[b], lane);
       }
       {
         V s[10];
         load_state<Q16, QMODE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
         const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
         consumed();
-        recon_halo<-1>(C, S.exch[b], lane);
+        recon_halo<1>(C, S.exch[b], lane);
       }
       mbar_arrive(&S.full[b][0]);
       // producer: once every warp has read plane it, its stage takes plane it + STAGES
@@ -485,6 +529,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       V (*exch)[kNW][32] = S.exch[b];
       mbar_wait(&S.bar[st], sph);
       V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
+      V zcen[3][3];  // [kx][az]: ky = 0 z-stage values of this source row (y centre term)
       {
         V s[10];
         load_state<Q16, QMODE>(S.stage[st], w, lane, plane_inflow(p), A, s);
@@ -493,50 +538,15 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         consumed();   // C depends on every loaded value
         // my slots of buffer b were read by my neighbours NB planes ago
         mbar_wait(&S.empty[b][w], eph ^ 1u);
-        V gz[3];
-        // cx = -1 -> dest q (final contribution)
-        const V c4 = vsplat(4.0f), cm4 = vsplat(-4.0f), c16 = vsplat(16.0f);
-        recon_row<-1>(C, exch, w, lane, gz);          // gz at 1/4 scale (cy = 0)
-        fin[0] = vfma(gz[0], c4, A9.a[0]);
-        fin[3] = vfma(gz[1], c4, A9.a[1]);
-        fin[9] = vfma(gz[2], c4, A9.a[2]);
-        fin[2] = A9.a[3];
-        fin[8] = A9.a[4];
-        fin[7] = A9.a[5];
-        fin[1] = vfma(gz[0], cm4, A9.b[0]);
-        fin[6] = vfma(gz[1], cm4, A9.b[1]);
-        fin[5] = A9.b[2];
-        fin[4] = vfma(gz[0], c4, A9.b[0]);
-        // cx = 0 -> dest p                          (gz at 1/16 scale: cx = 0 and cy = 0)
-        recon_row<0>(C, exch, w, lane, gz);
-        nb.b[0] = B6.a[0]; nb.b[1] = B6.a[1]; nb.b[2] = B6.a[3];
-        nb.a[0] = vfma(gz[0], c16, B6.a[0]);
-        nb.a[1] = vfma(gz[1], c16, B6.a[1]);
-        nb.a[2] = vfma(gz[2], c16, B6.a[2]);
-        nb.a[3] = B6.a[3]; nb.a[4] = B6.a[4]; nb.a[5] = B6.a[5];
-        // cx = +1 -> dest p+1                       (gz at 1/4 scale, folded after the y-stage)
-        recon_row<1>(C, exch, w, lane, gz);
-        nn.a[0] = gz[0]; nn.a[1] = gz[1]; nn.a[2] = gz[2];
+        recon_row<0>(C, exch, w, lane, zcen[0]);
+        recon_row<1>(C, exch, w, lane, zcen[1]);
+        recon_row<2>(C, exch, w, lane, zcen[2]);
       }
       if (++st == STAGES) { st = 0; sph ^= 1u; }
       mbar_arrive(&S.full[b][w]);
       mbar_wait(&S.full[b][wu], eph);
       mbar_wait(&S.full[b][wd], eph);
-      {
-        V t[3], d[2];
-        ystage<-1>(exch, w, lane, t, d);
-        fin[0] = vadd(fin[0], t[0]); fin[3] = vadd(fin[3], t[1]); fin[9] = vadd(fin[9], t[2]);
-        fin[2] = vadd(fin[2], d[0]); fin[8] = vadd(fin[8], d[1]); fin[7] = vadd(fin[7], t[0]);
-        fin[1] = vsub(fin[1], t[0]); fin[6] = vsub(fin[6], t[1]); fin[5] = vsub(fin[5], d[0]);
-        fin[4] = vadd(fin[4], t[0]);
-        ystage<0>(exch, w, lane, t, d);       // cx = 0 slots are at 1/4 scale
-        const V c4 = vsplat(4.0f);
-        nb.a[0] = vfma(t[0], c4, nb.a[0]); nb.a[1] = vfma(t[1], c4, nb.a[1]); nb.a[2] = vfma(t[2], c4, nb.a[2]);
-        nb.a[3] = vfma(d[0], c4, nb.a[3]); nb.a[4] = vfma(d[1], c4, nb.a[4]); nb.a[5] = vfma(t[0], c4, nb.a[5]);
-        ystage<1>(exch, w, lane, t, d);
-        nn.a[0] = vfma(nn.a[0], c4, t[0]); nn.a[1] = vfma(nn.a[1], c4, t[1]); nn.a[2] = vfma(nn.a[2], c4, t[2]);
-        nn.a[3] = d[0]; nn.a[4] = d[1]; nn.a[5] = t[0];
-      }
+      yx_stage(exch, wu, wd, lane, zcen, A9, B6, fin, nb, nn);
       mbar_arrive(&S.empty[b][wu]);
       mbar_arrive(&S.empty[b][wd]);
       if (store_plane) {
