@@ -189,7 +189,7 @@ __device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], 
 // halo row: only the y sum that enters the tile (S = 0: row y0-1 sends Yp up; S = 1: row
 // y0+15 sends Ym down), into the exchange slots of "row" 0
 template <int S>
-__device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32], int lane) {
+__device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32], int xrow, int lane) {
 #define HLBM_HALO_KX(KX)                                  \
   {                                                       \
     V Z[3][3];                                            \
@@ -197,7 +197,7 @@ __device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32],
     _Pragma("unroll") for (int az = 0; az < 3; ++az) {    \
       V p, m;                                             \
       ysums<KX>(Z, az, p, m);                             \
-      exch[xslot(KX, S, az)][0][lane] = S == 0 ? p : m;   \
+      exch[xslot(KX, S, az)][xrow][lane] = S == 0 ? p : m; \
     }                                                     \
   }
   HLBM_HALO_KX(0) HLBM_HALO_KX(1) HLBM_HALO_KX(2)
@@ -441,7 +441,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
   const int y0 = yt * kRows;                // first interior row; the box starts at storage row y0
   const int yrow = y0 + w - 1;              // logical y of this warp's row (row warps 1..15)
   const int zc = zs0 - kZOff + 2 * lane;    // logical z of this lane's .x cell (even)
-  const bool wr = (w >= 1) && (yrow < g.ny) && (lane >= 1) && (lane <= 30) && (zc < g.nz);
+  const bool row_warp = (w >= 1) && (w <= kRows);
+  const bool wr = row_warp && (yrow < g.ny) && (lane >= 1) && (lane <= 30) && (zc < g.nz);
   const int xs = g.xb + xsi * g.xseg, xe = min(xs + g.xseg, g.xr);
   const int NP = xe - xs + 2;
   const bool lo_inflow = g.x_lo_src < 0, hi_inflow = g.x_hi_src < 0;
@@ -457,7 +458,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     for (int b = 0; b < NB; ++b)
       for (int v = 0; v < kNW; ++v) {
         mbar_init(&S.full[b][v], 32);
-        mbar_init(&S.empty[b][v], 32 * (v == 0 ? 2 : (v + 1 <= kNW - 1) + (v - 1 >= 1)));
+        const int readers = (v == 0) ? (kHaloWarps == 1 ? 2 : 1)
+                            : (v > kRows ? 1 : (v + 1 <= kRows) + (v - 1 >= 1));
+        mbar_init(&S.empty[b][v], 32 * readers);
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
@@ -479,30 +482,34 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 #pragma unroll
     for (int k = 0; k < 5; ++k) acc[32 * k] = 0.f;
   }
-  if (w == 0) {
-    // ---- halo warp: the populations entering the tile from rows y0-1 and y0+15
+  if (!row_warp) {
+    // ---- halo warp(s): the populations entering the tile from rows y0-1 (Yp slots of exchange
+    // row 0) and y0+kRows (Ym slots of row 0, or of row 15 with a second halo warp)
+    const bool do_lo = (w == 0), do_hi = (kHaloWarps == 1) || (w == kNW - 1);
+    const int xrow = (kHaloWarps == 1) ? 0 : w;   // exchange row written by this warp
     for (int it = 0; it < NP; ++it) {
       const int b = (NB == 2) ? (it & 1) : 0;
       const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
       const bool inflow = plane_inflow(xs - 1 + it);
       mbar_wait(&S.bar[st], sph);
-      mbar_wait(&S.empty[b][0], eph ^ 1u);
-      {
+      mbar_wait(&S.empty[b][xrow], eph ^ 1u);
+      if (do_lo) {
         V s[10];
         load_state<Q16, QMODE>(S.stage[st], 0, lane, inflow, A, s);
         const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
-        recon_halo<0>(C, S.exch[b], lane);
+        if (!do_hi) consumed();
+        recon_halo<0>(C, S.exch[b], 0, lane);
       }
-      {
+      if (do_hi) {
         V s[10];
         load_state<Q16, QMODE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
         const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
         consumed();
-        recon_halo<1>(C, S.exch[b], lane);
+        recon_halo<1>(C, S.exch[b], xrow, lane);
       }
-      mbar_arrive(&S.full[b][0]);
-      // producer: once every warp has read plane it, its stage takes plane it + STAGES
-      if (lane == 0 && it + STAGES < NP) {
+      mbar_arrive(&S.full[b][xrow]);
+      // producer (warp 0): once every warp has read plane it, its stage takes plane it + STAGES
+      if (w == 0 && lane == 0 && it + STAGES < NP) {
         mbar_wait(&S.cons[st], sph);
         issue_plane<NC>(A, xs - 1 + it + STAGES, S.stage[st], &S.bar[st], zs0, y0);
       }

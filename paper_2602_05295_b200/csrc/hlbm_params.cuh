@@ -17,8 +17,12 @@
 
 namespace hlbm {
 
-constexpr int kNW = 16;          // warps per CTA: 1 halo warp + one warp per interior y row
-constexpr int kRows = kNW - 1;   // interior rows per tile
+#ifndef HLBM_HALO_WARPS
+#define HLBM_HALO_WARPS 1
+#endif
+constexpr int kNW = 16;          // warps per CTA: halo warp(s) + one warp per interior y row
+constexpr int kHaloWarps = HLBM_HALO_WARPS;   // 1: warp 0 does both halo rows; 2: warps 0 and 15
+constexpr int kRows = kNW - kHaloWarps;   // interior rows per tile
 constexpr int kBoxRows = kRows + 2;   // rows of a plane tile in shared memory (+1 halo row per side)
 constexpr int kZW = 64;          // z cells covered by one warp (32 lanes x 2 cells)
 constexpr int kZT = 60;          // interior z cells per tile (lanes 1..30; lanes 0 and 31 are halo)

@@ -7,9 +7,9 @@ cd "$(dirname "$0")/../paper_2602_05295_b200/csrc"
 out=../../diag/$name; mkdir -p $out
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --extended-lambda -Xcompiler -fPIC"
 objs=""
-for f in hlbm_interior hlbm_interior_q0 hlbm_interior_q1 hlbm_interior_q2; do
+for f in hlbm_interior hlbm_interior_q0 hlbm_interior_q1 hlbm_interior_q2 hlbm_cells hlbm_mesh hlbm_capi; do
   nvcc $FL "$@" -c $f.cu -o $out/$f.o & objs="$objs $out/$f.o"
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libhlbm.so $objs build/hlbm_cells.o build/hlbm_mesh.o build/hlbm_capi.o -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libhlbm.so $objs -lcudart
 echo built $out/libhlbm.so
