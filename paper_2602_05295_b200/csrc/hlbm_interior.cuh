@@ -25,6 +25,9 @@
 //     layers of the layout make every tile in-bounds (no wrap).
 #pragma once
 #include "hlbm_params.cuh"
+#ifndef HLBM_ABL_NOSAT
+#define HLBM_ABL_NOSAT 0
+#endif
 
 
 namespace hlbm {
@@ -349,15 +352,54 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
       }
     }
     V t[10];
-    float lo0 = 1e30f, hi0 = -1e30f, lo1 = 1e30f, hi1 = -1e30f;
 #pragma unroll
-    for (int c = 0; c < 10; ++c) {
+    for (int c = 0; c < 10; ++c)
       t[c] = vfma(s[c], vsplat(q_enc_scale<QMODE>(A.Q, c)), vsplat(q_enc_off<QMODE>(A.Q, c)));
-      if (STATS && B16) {   // every component maps [min, max] onto [0.5, 65535.5]
-        lo0 = fminf(lo0, t[c].x); hi0 = fmaxf(hi0, t[c].x);
-        lo1 = fminf(lo1, t[c].y); hi1 = fmaxf(hi1, t[c].y);
+    if (STATS && !HLBM_ABL_NOSAT) {
+      // saturation counters: m outside [min, max]  (checked before the dither is added)
+      bool satx, saty;
+      if (B16) {   // every component maps [min, max] onto [0.5, 65535.5]: two min/max trees
+        const float lo0 = fminf(fminf(fminf(fminf(t[0].x, t[1].x), fminf(t[2].x, t[3].x)),
+                                      fminf(fminf(t[4].x, t[5].x), fminf(t[6].x, t[7].x))), fminf(t[8].x, t[9].x));
+        const float hi0 = fmaxf(fmaxf(fmaxf(fmaxf(t[0].x, t[1].x), fmaxf(t[2].x, t[3].x)),
+                                      fmaxf(fmaxf(t[4].x, t[5].x), fmaxf(t[6].x, t[7].x))), fmaxf(t[8].x, t[9].x));
+        const float lo1 = fminf(fminf(fminf(fminf(t[0].y, t[1].y), fminf(t[2].y, t[3].y)),
+                                      fminf(fminf(t[4].y, t[5].y), fminf(t[6].y, t[7].y))), fminf(t[8].y, t[9].y));
+        const float hi1 = fmaxf(fmaxf(fmaxf(fmaxf(t[0].y, t[1].y), fmaxf(t[2].y, t[3].y)),
+                                      fmaxf(fmaxf(t[4].y, t[5].y), fmaxf(t[6].y, t[7].y))), fmaxf(t[8].y, t[9].y));
+        satx = statx && !(lo0 >= 0.5f && hi0 <= 65535.5f);   // NaN counts as saturated
+        saty = staty && !(lo1 >= 0.5f && hi1 <= 65535.5f);
+        if (satx || saty) {   // rare: per-component counts from the same t
+#pragma unroll
+          for (int c = 0; c < 10; ++c) {
+            const unsigned n = (satx && !(t[c].x >= 0.5f && t[c].x <= 65535.5f)) +
+                               (saty && !(t[c].y >= 0.5f && t[c].y <= 65535.5f));
+            if (n) atomicAdd(&A.stats->sat[c], (unsigned long long)n);
+          }
+        }
+      } else {     // generic bit widths: |r| > 1 with r = (m - mid) / half
+        float mx0 = 0.f, mx1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+          mx0 = fmaxf(mx0, fabsf(r.x));
+          mx1 = fmaxf(mx1, fabsf(r.y));
+        }
+        satx = statx && !(mx0 <= 1.0f);
+        saty = staty && !(mx1 <= 1.0f);
+        if (satx || saty) {
+#pragma unroll
+          for (int c = 0; c < 10; ++c) {
+            const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
+            const unsigned n = (satx && !(fabsf(r.x) <= 1.0f)) + (saty && !(fabsf(r.y) <= 1.0f));
+            if (n) atomicAdd(&A.stats->sat[c], (unsigned long long)n);
+          }
+        }
       }
-      if (DITHER) t[c] = vadd(t[c], nz[c]);
+    }
+    if (DITHER) {
+#pragma unroll
+      for (int c = 0; c < 10; ++c) t[c] = vadd(t[c], nz[c]);
     }
     uint2 wd[5];
 #pragma unroll
@@ -376,32 +418,6 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     }
     put_pair(g, reinterpret_cast<uint32_t*>(A.out) + cell_off, reinterpret_cast<uint32_t*>(A.out) + plane_off, y,
              z, wd, 5);
-    if (STATS) {
-      // saturation: |r| > 1  <=>  m outside [min, max]  (rare slow path)
-      bool satx, saty;
-      if (B16) {
-        satx = statx && (lo0 < 0.5f || hi0 > 65535.5f || hi0 != hi0);
-        saty = staty && (lo1 < 0.5f || hi1 > 65535.5f || hi1 != hi1);
-      } else {
-        float mx0 = 0.f, mx1 = 0.f;
-#pragma unroll
-        for (int c = 0; c < 10; ++c) {
-          const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
-          mx0 = fmaxf(mx0, fabsf(r.x));
-          mx1 = fmaxf(mx1, fabsf(r.y));
-        }
-        satx = statx && !(mx0 <= 1.0f);
-        saty = staty && !(mx1 <= 1.0f);
-      }
-      if (satx || saty) {
-#pragma unroll
-        for (int c = 0; c < 10; ++c) {
-          const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
-          const unsigned n = (satx && !(fabsf(r.x) <= 1.0f)) + (saty && !(fabsf(r.y) <= 1.0f));
-          if (n) atomicAdd(&A.stats->sat[c], (unsigned long long)n);
-        }
-      }
-    }
   }
   if (STATS) {
     // mass, momentum, max |u|^2 (NaN in any cell already makes the mass sum non-finite)
