@@ -117,6 +117,10 @@ int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats);
 int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out);
 /* full-grid update with the per-cell pull kernel (GPU reference for the fast kernel) */
 int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps);
+/* the original fused HOME-LBM step (Alg. 1): one kernel, one thread per
+ * cell, 27-link pull with voxel solid links resolved inline (bounce-back, solid cells at rest);
+ * the in-repo baseline of the split-scheme attribution.  Voxel solids only. */
+int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
 
 /* boundary list: global linear cell indices (sorted) and link masks; cells==NULL -> count only */
 int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n);

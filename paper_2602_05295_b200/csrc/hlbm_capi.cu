@@ -44,6 +44,7 @@ struct hlbm_ctx {
   int64_t ns = 0;
   uint32_t* d_bits = nullptr;
   int bits_row_words = 0;
+  uint32_t* d_fused = nullptr;   // dense per-cell mask of the fused Alg.-1 step (voxel solids)
   MeshLinks mesh;                // triangle-mesh cut links (replaces the voxel lists when set)
   float solid_v[3] = {0, 0, 0}, solid_w[3] = {0, 0, 0}, solid_c[3] = {0, 0, 0};
   std::vector<int64_t> off_b, off_s, off_m;   // per-plane offsets (nx+1) into the sorted lists
@@ -371,6 +372,7 @@ void hlbm_destroy(hlbm_ctx* ctx) {
   cudaFree(ctx->d_bmasks);
   cudaFree(ctx->d_scells);
   cudaFree(ctx->d_bits);
+  cudaFree(ctx->d_fused);
   free_mesh(ctx);
   for (int i = 0; i < 3; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -608,6 +610,10 @@ int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, c
   MaskGeo mg{c.nx, c.ny, c.nz, c.bc[2] == HLBM_BC_WALL, c.bc[3] == HLBM_BC_WALL, c.bc[4] == HLBM_BC_WALL,
              c.bc[5] == HLBM_BC_WALL};
   CK(launch_classify(d_ext, mg, d_links, d_cls, ctx->stream));
+  cudaFree(ctx->d_fused);
+  ctx->d_fused = nullptr;
+  CK(cudaMalloc(&ctx->d_fused, n * 4));
+  CK(launch_fused_masks(d_links, d_cls, n, ctx->d_fused, ctx->stream));
   for (int pass = 0; pass < 2; ++pass) {
     const uint8_t want = pass == 0 ? 1 : 2;
     CK(launch_compact(d_cls, d_links, n, want, d_counts, d_total, nullptr, nullptr, true, ctx->stream));
@@ -661,6 +667,7 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
     if (!std::isfinite(vertices[k])) return fail(ctx, HLBM_EINVAL, "non-finite vertex");
   const hlbm_config& c = ctx->cfg;
   // the mesh replaces any voxel lists
+  cudaFree(ctx->d_fused); ctx->d_fused = nullptr;
   cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
   cudaFree(ctx->d_bmasks); ctx->d_bmasks = nullptr;
   cudaFree(ctx->d_scells); ctx->d_scells = nullptr;
@@ -787,6 +794,33 @@ int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return HLBM_OK;
+}
+
+int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
+  if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the fused step supports voxel solids only");
+  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
+  const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
+  float tf = 0.f;
+  for (int s = 0; s < nsteps; ++s) {
+    const int st = (s == nsteps - 1) ? 1 : 0;
+    if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+    StepArgs A = make_args(ctx, st);
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    CK(launch_pull_cells(A, nullptr, ctx->d_fused, n, 3, q16, force, dither, ctx->stream));
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    ++ctx->launches;
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    float a = 0.f;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    tf += a;
+    ctx->cur = 1 - ctx->cur;
+    ++ctx->steps;
+  }
+  if (nsteps == 0) return HLBM_OK;
+  ctx->last_t_fluid = tf / nsteps;
+  ctx->last_t_solid = 0.0;
+  return hlbm_read_stats(ctx, out);
 }
 
 int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {

@@ -204,7 +204,10 @@ __device__ __forceinline__ void flush_stats(const StepArgs& A, float red[5]) {
 }
 
 // MODE 0: pull update of listed (or all) cells with voxel bounce-back on masked links;
-// MODE 1: reset listed solid cells to rest; MODE 2: mesh links (Eq. 8) + momentum exchange
+// MODE 1: reset listed solid cells to rest; MODE 2: mesh links (Eq. 8) + momentum exchange;
+// MODE 3: the fused single-kernel step (Alg. 1, original HOME-LBM): every cell of the
+//         slab, one thread each, 27-link pull with the solid links resolved inline from a dense
+//         per-cell mask (bit 0: the cell is solid -> rest; bits 1..26: cut links -> bounce-back)
 template <bool Q16, bool FORCE, bool DITHER, int MODE>
 __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepArgs A,
                                                   const int64_t* __restrict__ cells,
@@ -221,11 +224,12 @@ __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepAr
     const int64_t r = cell - (int64_t)x * yz;
     const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
     float s[10];
-    if (MODE == 1) {
+    const uint32_t fmask = (MODE == 3 && masks) ? masks[idx] : 0u;
+    if (MODE == 1 || (MODE == 3 && (fmask & 1u))) {
 #pragma unroll
       for (int c = 0; c < 10; ++c) s[c] = 0.f;
     } else {
-      const uint32_t mask = masks ? masks[idx] : 0u;
+      const uint32_t mask = MODE == 3 ? fmask : (masks ? masks[idx] : 0u);
       if (MODE == 2) {
         float o[10];
         load_cell<Q16>(A, x + 1, y, z, o);
@@ -241,10 +245,10 @@ __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepAr
       float m[10];
 #pragma unroll
       for (int c = 0; c < 10; ++c) m[c] = 0.f;
-      PullAll<0, Q16, FORCE, MODE>::run(A, x, y, z, mask, m, mc);
+      PullAll<0, Q16, FORCE, MODE == 3 ? 0 : MODE>::run(A, x, y, z, mask, m, mc);
       raw_to_state<float>(m, s);
     }
-    store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && MODE != 1, red);
+    store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && MODE != 1 && !(MODE == 3 && (fmask & 1u)), red);
   }
   if (A.do_stats && MODE != 1) flush_stats(A, red);
   if (MODE == 2 && A.do_stats) {
@@ -272,7 +276,8 @@ cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uin
   if (q16 == Q && force == F && dither == D) {                                                  \
     if (mode == 0) pull_cells<Q, F, D, 0><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);   \
     else if (mode == 1) pull_cells<Q, F, D, 1><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n); \
-    else pull_cells<Q, F, D, 2><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);             \
+    else if (mode == 2) pull_cells<Q, F, D, 2><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n); \
+    else pull_cells<Q, F, D, 3><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);             \
     return cudaGetLastError();                                                                  \
   }
   HLBM_PULL(false, false, false)
@@ -317,6 +322,19 @@ __global__ void classify_cells(const uint8_t* __restrict__ mask_ext, MaskGeo m,
     links[i] = lm;
     cls[i] = (uint8_t)((lm != 0 ? 1 : 0) | (solid ? 2 : 0));
   }
+}
+
+// dense per-cell mask of the fused step: link bits of fluid cells, bit 0 for solid cells
+__global__ void fused_masks_kernel(const uint32_t* __restrict__ links, const uint8_t* __restrict__ cls, int64_t n,
+                                   uint32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = links[i] | ((cls[i] & 2u) ? 1u : 0u);
+}
+
+cudaError_t launch_fused_masks(const uint32_t* links, const uint8_t* cls, int64_t n, uint32_t* out,
+                               cudaStream_t st) {
+  fused_masks_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(links, cls, n, out);
+  return cudaGetLastError();
 }
 
 constexpr int kCompactTPB = 256;

@@ -31,7 +31,8 @@ cudaError_t launch_bits_from_list(const int64_t* cells, int64_t n, int nz, int r
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
                                   int qmode, cudaStream_t st);
 // mode 0: voxel bounce-back on masked links; 1: reset listed solid cells to rest;
-// 2: triangle mesh, Eq.-8 boundary populations on masked links (t table in A.cut_t)
+// 2: triangle mesh, Eq.-8 boundary populations on masked links (t table in A.cut_t);
+// 3: fused single-kernel step over all cells with a dense per-cell mask (Alg. 1 baseline)
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
@@ -40,6 +41,8 @@ cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, co
 cudaError_t launch_export(const Geo& g, const Ranges& R, bool q16, const void* src, double* rho,
                           double* mom, double* stress, int x0, int cx, int y0, int cy, int z0, int cz,
                           cudaStream_t st);
+cudaError_t launch_fused_masks(const uint32_t* links, const uint8_t* cls, int64_t n, uint32_t* out,
+                               cudaStream_t st);
 cudaError_t launch_classify(const uint8_t* mask_ext, const MaskGeo& m, uint32_t* links, uint8_t* cls,
                             cudaStream_t st);
 int64_t compact_tiles(int64_t n);

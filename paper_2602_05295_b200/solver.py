@@ -282,6 +282,15 @@ class Solver:
         self._chk(self._lib.hlbm_read_stats(self._ctx, C.byref(s)))
         return StepStats._from_c(s)
 
+    def step_fused(self, n: int = 1) -> StepStats:
+        """The original fused HOME-LBM step (Alg. 1): one kernel, one thread per cell,
+        solid links resolved inline -- the in-repo baseline of the split scheme (voxel solids)."""
+        self.state_version += 1
+        s = _lib.HlbmStats()
+        self._chk(self._lib.hlbm_step_fused(self._ctx, int(n), C.byref(s)))
+        self._last = StepStats._from_c(s)
+        return self._last
+
     def step_reference(self, n: int = 1):
         """Full-grid update with the per-cell pull kernel (GPU cross-check of the fast kernel)."""
         self.state_version += 1

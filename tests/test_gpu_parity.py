@@ -225,3 +225,52 @@ def test_q16_saturation_counts():
     assert clear > 0
     assert clear <= st.saturation[0] <= loose
     assert np.all(st.saturation[1:] == 0)
+
+
+@pytest.mark.parametrize("bcname", ["channel", "closed"])
+def test_fused_alg1_step_matches_oracle_and_split(bcname):
+    """The fused single-kernel step (Alg. 1 baseline, solid links inline) against the
+    oracle (fp32 tolerance) and against the split scheme (interior kernel + compacted boundary
+    kernel): the two schemes compute the same step."""
+    shape = (40, 24, 28)
+    mask = sphere_mask(shape, (14, 11.5, 13.5), 5)
+    if bcname == "channel":
+        bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("wall", "wall")}
+    else:
+        bc = {"x": ("wall", "wall"), "y": ("wall", "wall"), "z": ("wall", "wall")}
+    cfg = SolverConfig(nu=0.02, bc=bc, u_in=(0.05, 0, 0))
+    obc = OS.BC(x=bc["x"], y=bc["y"], z=bc["z"], u_in=(0.05, 0, 0))
+    state = _channel_state(shape, mask, 0.05)
+    res = {}
+    for scheme in ("fused", "split"):
+        with Solver(SimGrid(shape, mask), cfg) as s:
+            s.set_moments(*state)
+            st = s.step_fused(5) if scheme == "fused" else s.step(5)
+            res[scheme] = (s.moments(), st)
+    ref = state
+    for _ in range(5):
+        ref = OS.fluid_step(*ref, cfg.tau, obc, None, mask)
+    fl = ~mask.astype(bool)
+    assert max(moment_errors(res["fused"][0], ref, fl)) <= FP32_TOL
+    assert max(moment_errors(res["fused"][0], res["split"][0], fl)) <= FP32_TOL
+    assert np.all(res["fused"][0][0][~fl] == 1.0) and np.all(res["fused"][0][1][:, ~fl] == 0.0)
+    assert res["fused"][1].mass == pytest.approx(res["split"][1].mass, rel=1e-7)
+
+
+def test_fused_alg1_q16_matches_split_within_1_lsb():
+    shape = (32, 20, 24)
+    mask = sphere_mask(shape, (12, 9.5, 11.5), 4)
+    bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("periodic", "periodic")}
+    cfg = SolverConfig(nu=0.02, bc=bc, u_in=(0.05, 0, 0), precision="q16", quant=QuantSpec())
+    state = _channel_state(shape, mask, 0.05)
+    words = {}
+    for scheme in ("fused", "split"):
+        with Solver(SimGrid(shape, mask), cfg) as s:
+            s.set_moments(*state)
+            if scheme == "fused":
+                s.step_fused(1)
+            else:
+                s.step(1)
+            words[scheme] = s.codes
+    d = np.abs(codec.unpack(words["fused"]).astype(np.int64) - codec.unpack(words["split"]).astype(np.int64))
+    assert d.max() <= 1

@@ -5,7 +5,9 @@ config 2: turbulence box 512^3, fp32 and q16 (bench.py's headline)
 config 3: channel past a sphere 512x256x256 (inflow/outflow, periodic y/z), fp32 and q16
 config 4: procedural vehicle 1000x400x400, q16 + dither, inflow/outflow, periodic y/z
 Prints one JSON object per line: MLUPS (all cells), fluid-cell MLUPS, the split phase times
-(fluid_interior vs compacted boundary kernel) and boundary-list sizes.
+(fluid_interior vs compacted boundary kernel), boundary-list sizes and, for voxel scenes, the
+time of the fused single-kernel Alg.-1 baseline -- the in-repo version of
+the paper's split / quantization attribution.
 """
 import json
 import sys
@@ -42,6 +44,10 @@ def run(name, dims, cfg, init, mask=None, steps=50, mesh=None):
     s.step_async(5)
     ms = timed(s, steps)
     st = s.step(3)              # phase split (events around each kernel) + stats
+    fused_ms = None
+    if mesh is None:            # the fused Alg.-1 baseline (one kernel, solid links inline)
+        s.step_fused(1)
+        fused_ms = s.step_fused(max(2, steps // 10)).t_fluid_ms
     cells = int(np.prod(dims))
     nb = len(s.boundary_cells) if mask is not None else (len(s.cut_links()[0]) if mesh is not None else 0)
     out = {"config": name, "dims": list(dims), "precision": cfg.precision, "ms_per_step": round(ms, 4),
@@ -50,6 +56,9 @@ def run(name, dims, cfg, init, mask=None, steps=50, mesh=None):
            "boundary_cells": nb, "solid_cells": cells - st.n_fluid, "setup_s": round(setup, 2),
            "triangles": 0 if mesh is None else int(len(mesh[1])),
            "max_u": round(st.max_u, 4), "saturation_rho": int(st.saturation[0])}
+    if fused_ms is not None:
+        out["fused_alg1_ms_per_step"] = round(fused_ms, 4)
+        out["split_speedup_vs_fused"] = round(fused_ms / ms, 2)
     s.close()
     print(json.dumps(out), flush=True)
 
