@@ -228,12 +228,14 @@ __device__ __forceinline__ void raw_to_state(const T m[10], T out[10], T* inv_ou
   out[1] = jx;
   out[2] = jy;
   out[3] = jz;
-  out[4] = vsub(vsub(m[4], d3), vmul(jx, ux));
-  out[5] = vsub(m[5], vmul(jx, uy));
-  out[6] = vsub(m[6], vmul(jx, uz));
-  out[7] = vsub(vsub(m[7], d3), vmul(jy, uy));
-  out[8] = vsub(m[8], vmul(jy, uz));
-  out[9] = vsub(vsub(m[9], d3), vmul(jz, uz));
+  // sneq = Pi - d/3 delta - j u, the j u products fused into the subtraction (one rounding)
+  const T njx = vneg(jx), njy = vneg(jy), njz = vneg(jz);
+  out[4] = vfma(njx, ux, vsub(m[4], d3));
+  out[5] = vfma(njx, uy, m[5]);
+  out[6] = vfma(njx, uz, m[6]);
+  out[7] = vfma(njy, uy, vsub(m[7], d3));
+  out[8] = vfma(njy, uz, m[8]);
+  out[9] = vfma(njz, uz, vsub(m[9], d3));
 }
 
 // ------------------------------------------------------------------ 16-bit codec
