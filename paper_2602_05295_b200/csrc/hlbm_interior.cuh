@@ -92,15 +92,13 @@ __device__ __forceinline__ void issue_plane(const StepArgs& A, int p, uint32_t (
   tma_load_4d(&stage[0][0][0], &A.tmap_in, zs0, ys0, 0, sp, bar);
 }
 
-// Partial moments of one destination plane.  Index order of the 6 "kx=0" moments:
-// (ky,kz) = 00, 01, 02, 10, 11, 20.  A plane that has received the cx=+1 contribution
-// of source q-1 and the cx=0 contribution of source q carries 9 values (a: kx=0,
-// b: kx=1 for (ky,kz) = 00, 01, 10; the kx=2 partial equals b[0]).
-struct Part9 {
-  V a[6];
-  V b[3];
-};
-struct Part6 {   // only the cx=+1 contribution of source q-1: kx=1/kx=2 partials are copies
+// Partial moments of one destination plane, index order of the 6 (ay,az) combinations
+// 00, 01, 02, 10, 11, 20.  The x march keeps, per destination plane, N = the cx=+1 contribution
+// of source q-1 (identical for every ax) and M = N + the cx=0 contribution of source q (ax = 0);
+// the ax = 1 / ax = 2 partials of plane q are N's 00, 01, 10 entries.  N of plane q is read for
+// the last time in the iteration that creates N of plane q+2, which overwrites it in place, so
+// the x2-unrolled loop rotates two M and two N register sets without copying any partial.
+struct Part6 {
   V a[6];
 };
 
@@ -210,13 +208,14 @@ __device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32],
 // y pull + x stage of one destination row.  The exchange rows form a ring over the warps: row
 // warp w (1..15) reads the Yp slots of wu = w-1 and the Ym slots of wd = (w+1) mod 16, so the
 // first row reads the halo warp's row-(y0-1) values and the last its row-(y0+15) values.
-//   fin (dest q):   A9 (sources q-1, q) + x-pull of Xm from this source plane (cx = -1)
-//   nb  (dest p):   B6 (source p-1) + 4 Xc (cx = 0); kx=1 partials copied
-//   nn  (dest p+1): Xp (cx = +1), identical for every ax
+//   fin (dest q):   Mq (sources q-1, q), Nq (source q-1) + x-pull of Xm (cx = -1)
+//   nb  (dest p):   Np (source p-1) + 4 Xc (cx = 0)
+//   nn  (dest p+1): Xp (cx = +1), identical for every ax; written over Nq (combo by combo,
+//                   each Nq entry is read before its slot is rewritten)
 // Raw-moment order of fin: m000 m100 m010 m001 m200 m110 m101 m020 m011 m002; partial index
 // order (ay,az) = 00, 01, 02, 10, 11, 20 (b: 00, 01, 10).
 __device__ __forceinline__ void yx_stage(V (*exch)[kNW][32], int wu, int wd, int lane, const V zc[3][3],
-                                         const Part9& A9, const Part6& B6, V fin[10], Part9& nb, Part6& nn) {
+                                         const Part6& Mq, Part6& NqNn, const Part6& Np, V fin[10], Part6& nb) {
   const V c4 = vsplat(4.0f);
 #pragma unroll
   for (int az = 0; az < 3; ++az) {
@@ -237,16 +236,14 @@ __device__ __forceinline__ void yx_stage(V (*exch)[kNW][32], int wu, int wd, int
       const V P = vadd(Y[0][ay], Y[2][ay]);
       const V Xp = vadd(P, Y[1][ay]);
       const V Xm = vsub(P, Y[1][ay]);
-      fin[m0] = vadd(A9.a[c], Xm);
+      fin[m0] = vadd(Mq.a[c], Xm);
       if (ay + az <= 1) {
-        const int bi = ay == 0 ? az : 2;                            // b index of (ay, az)
         const int m1 = ay == 0 ? (az == 0 ? 1 : 6) : 5;
-        fin[m1] = vsub(A9.b[bi], Xm);
-        nb.b[bi] = B6.a[c];
+        fin[m1] = vsub(NqNn.a[c], Xm);
       }
-      if (ay + az == 0) fin[4] = vadd(A9.b[0], Xm);
-      nb.a[c] = vfma(Y[0][ay], c4, B6.a[c]);
-      nn.a[c] = Xp;
+      if (ay + az == 0) fin[4] = vadd(NqNn.a[0], Xm);
+      nb.a[c] = vfma(Y[0][ay], c4, Np.a[c]);
+      NqNn.a[c] = Xp;
     }
   }
 }
@@ -533,17 +530,15 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     }
   } else {
     // ---- row warps
-    Part9 Ac, Ad;   // dest p-1 partials (two register sets: the loop is unrolled x2)
-    Part6 Bc, Bd;   // dest p partials
+    Part6 Ma, Mb, Na, Nb;   // rotating plane partials (x2 unroll, see Part6)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) Ac.a[k] = Bc.a[k] = vsplat(0.f);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) Ac.b[k] = vsplat(0.f);
+    for (int k = 0; k < 6; ++k) Ma.a[k] = Na.a[k] = Nb.a[k] = vsplat(0.f);
     const int wu = w - 1, wd = (w + 1) & (kNW - 1);   // exchange rows read by this warp
     const int64_t cell0 = (int64_t)(yrow + 1) * g.zp + (zc + kZOff);   // pair offset inside a plane
 
-    // one source plane: (A9, B6) carried in, (nb, nn) carried out
-    auto body = [&](const int it, const Part9& A9, const Part6& B6, Part9& nb, Part6& nn) {
+    // one source plane p: Mq, Nq (dest q = p-1), Np (dest p) carried in; nb = M of dest p and
+    // N of dest p+1 (written over Nq) carried out
+    auto body = [&](const int it, const Part6& Mq, Part6& NqNn, const Part6& Np, Part6& nb) {
       const int p = xs - 1 + it;
       const int q = p - 1;   // destination plane finished in this iteration
       const bool store_plane = wr && it >= 2;
@@ -569,7 +564,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       mbar_arrive(&S.full[b][w]);
       mbar_wait(&S.full[b][wu], eph);
       mbar_wait(&S.full[b][wd], eph);
-      yx_stage(exch, wu, wd, lane, zcen, A9, B6, fin, nb, nn);
+      yx_stage(exch, wu, wd, lane, zcen, Mq, NqNn, Np, fin, nb);
       mbar_arrive(&S.empty[b][wu]);
       mbar_arrive(&S.empty[b][wd]);
       if (store_plane) {
@@ -585,8 +580,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
     };
 
     for (int it = 0; it < NP; it += 2) {
-      body(it, Ac, Bc, Ad, Bd);
-      if (it + 1 < NP) body(it + 1, Ad, Bd, Ac, Bc);
+      body(it, Ma, Nb, Na, Mb);
+      if (it + 1 < NP) body(it + 1, Mb, Na, Nb, Ma);
     }
   }
 
