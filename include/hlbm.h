@@ -61,7 +61,7 @@ typedef struct hlbm_config {
 /* StepStats. Sums run over fluid cells of this slab. */
 typedef struct hlbm_stats {
   int64_t step;
-  double t_fluid_ms, t_copy_ms, t_solid_ms;
+  double t_fluid_ms, t_copy_ms, t_solid_ms;   /* device times of the last step of the call */
   double mass;
   double momentum[3];
   double max_u;

@@ -31,6 +31,7 @@ struct hlbm_ctx {
   void* buf[2] = {nullptr, nullptr};
   int cur = 0;
   Stats* d_stats = nullptr;
+  Stats* h_stats = nullptr;      // pinned host copy (one D2H per Solver.step, no extra sync)
   Relax R{};
   Codec Q{};
   Ranges RG{};
@@ -353,6 +354,7 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
   }
   CK(cudaMalloc(&ctx->d_stats, sizeof(Stats)));
   CK(cudaMemset(ctx->d_stats, 0, sizeof(Stats)));
+  CK(cudaMallocHost(&ctx->h_stats, sizeof(Stats)));
   for (int i = 0; i < 3; ++i) CK(cudaEventCreate(&ctx->ev[i]));
   // default state: rest (rho = 1, j = 0, sneq = 0) in both buffers
   for (int b = 0; b < 2; ++b) {
@@ -368,6 +370,7 @@ void hlbm_destroy(hlbm_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (int b = 0; b < 2; ++b) cudaFree(ctx->buf[b]);
   cudaFree(ctx->d_stats);
+  cudaFreeHost(ctx->h_stats);
   cudaFree(ctx->d_bcells);
   cudaFree(ctx->d_bmasks);
   cudaFree(ctx->d_scells);
@@ -823,11 +826,9 @@ int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   return hlbm_read_stats(ctx, out);
 }
 
-int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {
-  if (!ctx) return HLBM_EINVAL;
-  Stats h{};
-  CK(cudaMemcpyAsync(&h, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+// StepStats from the host copy of the device accumulators (ctx->h_stats, already synchronised)
+static int stats_from_host(hlbm_ctx* ctx, hlbm_stats* out) {
+  const Stats& h = *ctx->h_stats;
   const hlbm_config& c = ctx->cfg;
   const int64_t nfluid = (int64_t)c.nx * c.ny * c.nz - ctx->ns;
   float mu2;
@@ -854,31 +855,40 @@ int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {
   return HLBM_OK;
 }
 
+int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {
+  if (!ctx) return HLBM_EINVAL;
+  CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return stats_from_host(ctx, out);
+}
+
+// n steps; the statistics (and the phase times t_fluid / t_solid) are those of the last step.
+// One host synchronisation per call: the stats copy is enqueued behind the last kernel.
 int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
   if (nsteps == 0) {
     if (out) { memset(out, 0, sizeof(*out)); out->step = ctx->steps; out->finite = 1; }
     return HLBM_OK;
   }
-  double tf = 0, ts = 0;
   for (int s = 0; s < nsteps; ++s) {
-    const int st = (s == nsteps - 1) ? 1 : 0;
-    if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
-    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    if (int r = run_range(ctx, 0, ctx->cfg.nx, st, ctx->ev[1])) return r;
-    CK(cudaEventRecord(ctx->ev[2], ctx->stream));
-    CK(cudaEventSynchronize(ctx->ev[2]));
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
-    cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
-    tf += a;
-    ts += b;
+    const bool last = s == nsteps - 1;
+    if (last) {
+      CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+      CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    }
+    if (int r = run_range(ctx, 0, ctx->cfg.nx, last ? 1 : 0, last ? ctx->ev[1] : nullptr)) return r;
+    if (last) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->cur = 1 - ctx->cur;
     ++ctx->steps;
   }
-  ctx->last_t_fluid = tf / nsteps;
-  ctx->last_t_solid = ts / nsteps;
-  return hlbm_read_stats(ctx, out);
+  CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float a = 0.f, b = 0.f;
+  cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+  ctx->last_t_fluid = a;
+  ctx->last_t_solid = b;
+  return stats_from_host(ctx, out);
 }
 
 }  // extern "C"
