@@ -25,9 +25,6 @@
 //     layers of the layout make every tile in-bounds (no wrap).
 #pragma once
 #include "hlbm_params.cuh"
-#ifndef HLBM_ABL_NOSAT
-#define HLBM_ABL_NOSAT 0
-#endif
 
 
 namespace hlbm {
@@ -352,7 +349,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
 #pragma unroll
     for (int c = 0; c < 10; ++c)
       t[c] = vfma(s[c], vsplat(q_enc_scale<QMODE>(A.Q, c)), vsplat(q_enc_off<QMODE>(A.Q, c)));
-    if (STATS && !HLBM_ABL_NOSAT) {
+    if (STATS) {
       // saturation counters: m outside [min, max]  (checked before the dither is added)
       bool satx, saty;
       if (B16) {   // every component maps [min, max] onto [0.5, 65535.5]: two min/max trees
