@@ -1,4 +1,4 @@
-"""ORACLE (test infrastructure only) -- D3Q27 lattice tables.
+"""ORACLE (test infrastructure only) -- D3Q27 (and D3Q19) lattice tables.
 
 CPU restatement of the reference's lattice construction, used ONLY by
 ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
@@ -11,6 +11,10 @@ Restates ``/root/reference/pkg/src/momentlbm/lattice.py``:
   * Hermite tables h2 / h2c / h3 -- ``hermite2``/``hermite3``/``_build_hermite``
     (lattice.py:142-169); Voigt order xx,xy,xz,yy,yz,zz (lattice.py:23);
     third-order labels xxy,xyy,xxz,xzz,yzz,yyz,xyz (lattice.py:30).
+  * D3Q19 -- the first 19 directions of the same order (no corners, lattice.py:99-116),
+    weights 1/3, 1/18, 1/36 (``_WEIGHT_BY_SPEED2["D3Q19"]``, lattice.py:121), no xyz label
+    (lattice.py:166-167).  The module-level names are the D3Q27 tables; ``D3Q19`` / ``D3Q27``
+    / ``get(q)`` return the same tables as a ``Lat`` record.
 """
 
 from __future__ import annotations
@@ -74,6 +78,36 @@ for _j, _l in enumerate(VOIGT):
     if _l[0] != _l[1]:
         H2C[:, _j] *= 2.0                                                   # lattice.py:159-162
 H3 = np.stack([_h3(_CF, l) for l in H3_LABELS], axis=1)                     # (27, 7)
+
+
+class Lat:
+    """One velocity set: C, Q, W, OPP, H2, H2C, H3, H3_LABELS."""
+
+    def __init__(self, q: int):
+        c = d3q27_velocities()[:q]
+        self.Q = q
+        self.C = c
+        wex = {27: _W_EXACT, 19: {0: Fraction(1, 3), 1: Fraction(1, 18), 2: Fraction(1, 36)}}[q]
+        self.W_EXACT = tuple(wex[int((v * v).sum())] for v in c)
+        self.W = np.array([float(x) for x in self.W_EXACT])
+        self.OPP = np.array([[int(j) for j in range(q) if (c[j] == -c[i]).all()][0] for i in range(q)],
+                            dtype=np.int64)
+        cf = c.astype(np.float64)
+        self.H2 = np.stack([_h2(cf, _AXIS[l[0]], _AXIS[l[1]]) for l in VOIGT], axis=1)
+        self.H2C = self.H2.copy()
+        for j, l in enumerate(VOIGT):
+            if l[0] != l[1]:
+                self.H2C[:, j] *= 2.0
+        self.H3_LABELS = H3_LABELS if q == 27 else tuple(l for l in H3_LABELS if l != "xyz")
+        self.H3 = np.stack([_h3(cf, l) for l in self.H3_LABELS], axis=1)
+
+
+D3Q27 = Lat(27)
+D3Q19 = Lat(19)
+
+
+def get(q=None) -> Lat:
+    return D3Q19 if q == 19 else D3Q27
 
 
 def voigt_index():

@@ -113,23 +113,24 @@ def padded_solid(mask, bc: BC):
     return m
 
 
-def link_masks_dense(mask, bc: BC):
+def link_masks_dense(mask, bc: BC, lat=None):
     """(nx,ny,nz) uint32: bit i set iff fluid cell x has a solid source x - c_i."""
+    lat = lat or L.D3Q27
     ps = padded_solid(mask, bc)
     nx, ny, nz = mask.shape
     out = np.zeros((nx, ny, nz), dtype=np.uint32)
-    for i in range(1, L.Q):
-        cx, cy, cz = L.C[i]
+    for i in range(1, lat.Q):
+        cx, cy, cz = lat.C[i]
         src = ps[1 - cx:1 - cx + nx, 1 - cy:1 - cy + ny, 1 - cz:1 - cz + nz]
         out |= (src.astype(np.uint32) << np.uint32(i))
     out[np.asarray(mask, dtype=bool)] = 0
     return out
 
 
-def boundary_lists(mask, bc: BC):
+def boundary_lists(mask, bc: BC, lat=None):
     """(cells int64 sorted by linear index, link masks uint32) -- fluid cells
     with at least one solid pull source."""
-    lm = link_masks_dense(mask, bc)
+    lm = link_masks_dense(mask, bc, lat)
     flat = lm.reshape(-1)
     cells = np.nonzero(flat)[0].astype(np.int64)
     return cells, flat[cells].astype(np.uint32)
@@ -141,44 +142,46 @@ def solid_cells(mask):
 
 # ---------------------------------------------------------------- the step
 
-def step_padded(padded, tau, force=None, link_solid=None):
+def step_padded(padded, tau, force=None, link_solid=None, lat=None):
     """One Alg.-2 update of a ghost-padded 10-component block.
 
     ``padded`` is (10, nx+2, ny+2, nz+2) in (rho, mom, stress) form; returns
     the (rho, mom, stress) of the nx*ny*nz interior.  ``link_solid`` is an
     optional (27, nx, ny, nz) bool array: True where the pull source of
     direction i is solid (half-way bounce-back replaces that population)."""
+    lat = lat or L.D3Q27
     rho, mom, stress = padded[0], padded[1:4], padded[4:10]
     r, m, s = collide_moments(rho, mom, stress, force, tau)       # collision.py:137
-    f = reconstruct_distributions(r, m, s)                          # moments.py:64
+    f = reconstruct_distributions(r, m, s, lat)                     # moments.py:64
     nx, ny, nz = (d - 2 for d in rho.shape)
-    fs = np.empty((L.Q, nx, ny, nz))
-    for i in range(L.Q):
-        cx, cy, cz = L.C[i]
+    fs = np.empty((lat.Q, nx, ny, nz))
+    for i in range(lat.Q):
+        cx, cy, cz = lat.C[i]
         # pull: f_i(x) <- f_i(x - c_i)
         fs[i] = f[i, 1 - cx:1 - cx + nx, 1 - cy:1 - cy + ny, 1 - cz:1 - cz + nz]
     if link_solid is not None:
         inner = f[:, 1:-1, 1:-1, 1:-1]
-        for i in range(1, L.Q):
+        for i in range(1, lat.Q):
             sel = link_solid[i]
             if sel.any():
-                fs[i][sel] = inner[L.OPP[i]][sel]
-    return moments_from_distributions(fs)                           # moments.py:25
+                fs[i][sel] = inner[lat.OPP[i]][sel]
+    return moments_from_distributions(fs, lat)                      # moments.py:25
 
 
-def fluid_step(rho, mom, stress, tau, bc: BC | None = None, force=None, mask=None):
-    """One fluid update of the whole grid in the reference layout."""
+def fluid_step(rho, mom, stress, tau, bc: BC | None = None, force=None, mask=None, lat=None):
+    """One fluid update of the whole grid in the reference layout (``lat``: D3Q27 default)."""
     bc = bc or BC()
+    lat = lat or L.D3Q27
     padded = pad_state(rho, mom, stress, bc)
     link_solid = None
     solid = None
     if mask is not None and np.any(mask) or _has_wall(bc):
         mask = np.zeros(rho.shape, dtype=bool) if mask is None else np.asarray(mask, dtype=bool)
-        lm = link_masks_dense(mask, bc)
-        link_solid = ((lm[None] >> np.arange(L.Q, dtype=np.uint32)[:, None, None, None])
+        lm = link_masks_dense(mask, bc, lat)
+        link_solid = ((lm[None] >> np.arange(lat.Q, dtype=np.uint32)[:, None, None, None])
                       & np.uint32(1)).astype(bool)
         solid = mask
-    r, m, s = step_padded(padded, tau, force, link_solid)
+    r, m, s = step_padded(padded, tau, force, link_solid, lat)
     if solid is not None and solid.any():
         r[solid] = 1.0
         m[:, solid] = 0.0
@@ -190,9 +193,9 @@ def _has_wall(bc: BC):
     return any(k == "wall" for k in bc.x + bc.y + bc.z)
 
 
-def run(rho, mom, stress, tau, steps, bc=None, force=None, mask=None):
+def run(rho, mom, stress, tau, steps, bc=None, force=None, mask=None, lat=None):
     for _ in range(steps):
-        rho, mom, stress = fluid_step(rho, mom, stress, tau, bc, force, mask)
+        rho, mom, stress = fluid_step(rho, mom, stress, tau, bc, force, mask, lat)
     return rho, mom, stress
 
 
@@ -200,14 +203,14 @@ def run(rho, mom, stress, tau, steps, bc=None, force=None, mask=None):
 
 def fluid_step_q16(words, tau, step_index, bc=None, force=None, mask=None,
                    mmin=codec.DEFAULT_MIN, mmax=codec.DEFAULT_MAX, bits=None,
-                   dither=False, seed=0, x0=0, global_shape=None):
+                   dither=False, seed=0, x0=0, global_shape=None, lat=None):
     """Reference quantized path: decode -> float64 step -> encode.
 
     Dither noise is keyed by the global linear cell index; ``x0`` and
     ``global_shape`` locate a slab inside the global grid."""
     rho, mom, sneq = codec.decode_state(words, mmin, mmax, bits)
     stress = neq_recompose(rho, mom, sneq)
-    r, m, s = fluid_step(rho, mom, stress, tau, bc, force, mask)
+    r, m, s = fluid_step(rho, mom, stress, tau, bc, force, mask, lat)
     n = neq_decompose(r, m, s)
     noise = None
     if dither:

@@ -29,6 +29,7 @@ class HlbmConfig(C.Structure):
         ("precision", C.c_int32),
         ("qmin", C.c_double * 10), ("qmax", C.c_double * 10), ("bits", C.c_int32 * 10),
         ("dither", C.c_int32), ("seed", C.c_uint32), ("device", C.c_int32), ("xseg", C.c_int32),
+        ("q", C.c_int32),
     ]
 
 

@@ -19,6 +19,7 @@ using namespace hlbm;
 struct hlbm_ctx {
   hlbm_config cfg{};
   int q16 = 0, NC = 10;
+  int q = 27;        // velocity set (D3Q19 steps with the per-cell fused kernel)
   bool b16 = true;   // every component uses all 16 bits of its slot
   int qmode = 0;     // interior-kernel codec variant (hlbm_launch.h)
   cudaStream_t stream = nullptr;
@@ -202,6 +203,15 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   StepArgs A = make_args(ctx, with_stats, xb, xr);
+  if (ctx->q == 19) {
+    // D3Q19: the per-cell fused kernel over the planes of the range, solid links inline
+    const int64_t pl = (int64_t)ctx->cfg.ny * ctx->cfg.nz;
+    CK(launch_pull_cells(A, nullptr, ctx->d_fused, (int64_t)(xr - xb) * pl, 3, q16, force, dither, ctx->stream, 19,
+                         (int64_t)xb * pl));
+    ++ctx->launches;
+    if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
+    return HLBM_OK;
+  }
   CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
   ++ctx->launches;
   if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
@@ -278,6 +288,9 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
       (c.bc[4] == HLBM_BC_PERIODIC) != (c.bc[5] == HLBM_BC_PERIODIC))
     return bad("periodic y/z needs both faces periodic");
   if (c.precision != HLBM_FP32 && c.precision != HLBM_Q16) return bad("unknown precision");
+  if (c.q == 0) c.q = 27;
+  if (c.q != 27 && c.q != 19) return bad("lattice must be D3Q27 or D3Q19");
+  ctx->q = c.q;
   ctx->q16 = c.precision == HLBM_Q16;
   ctx->NC = ctx->q16 ? 5 : 10;
   if (ctx->q16) {
@@ -611,7 +624,7 @@ int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, c
   CK(cudaMalloc(&d_total, 8));
   CK(cudaMemcpy(d_ext, ext.data(), ext.size(), cudaMemcpyHostToDevice));
   MaskGeo mg{c.nx, c.ny, c.nz, c.bc[2] == HLBM_BC_WALL, c.bc[3] == HLBM_BC_WALL, c.bc[4] == HLBM_BC_WALL,
-             c.bc[5] == HLBM_BC_WALL};
+             c.bc[5] == HLBM_BC_WALL, ctx->q};
   CK(launch_classify(d_ext, mg, d_links, d_cls, ctx->stream));
   cudaFree(ctx->d_fused);
   ctx->d_fused = nullptr;
@@ -669,6 +682,7 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
   for (int64_t k = 0; k < 3 * nv; ++k)
     if (!std::isfinite(vertices[k])) return fail(ctx, HLBM_EINVAL, "non-finite vertex");
   const hlbm_config& c = ctx->cfg;
+  if (ctx->q != 27) return fail(ctx, HLBM_EINVAL, "triangle meshes need the D3Q27 lattice");
   // the mesh replaces any voxel lists
   cudaFree(ctx->d_fused); ctx->d_fused = nullptr;
   cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
@@ -778,14 +792,14 @@ int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
   const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
   for (int s = 0; s < nsteps; ++s) {
     StepArgs A = make_args(ctx, 0);
-    CK(launch_pull_cells(A, nullptr, nullptr, n, 0, q16, force, dither, ctx->stream));
+    CK(launch_pull_cells(A, nullptr, nullptr, n, 0, q16, force, dither, ctx->stream, ctx->q));
     ++ctx->launches;
     if (ctx->nb) {
-      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream));
+      CK(launch_pull_cells(A, ctx->d_bcells, ctx->d_bmasks, ctx->nb, 0, q16, force, dither, ctx->stream, ctx->q));
       ++ctx->launches;
     }
     if (ctx->ns) {
-      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream));
+      CK(launch_pull_cells(A, ctx->d_scells, nullptr, ctx->ns, 1, q16, force, dither, ctx->stream, ctx->q));
       ++ctx->launches;
     }
     if (ctx->mesh.nb) {
@@ -810,7 +824,7 @@ int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    CK(launch_pull_cells(A, nullptr, ctx->d_fused, n, 3, q16, force, dither, ctx->stream));
+    CK(launch_pull_cells(A, nullptr, ctx->d_fused, n, 3, q16, force, dither, ctx->stream, ctx->q));
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     ++ctx->launches;
     CK(cudaEventSynchronize(ctx->ev[1]));

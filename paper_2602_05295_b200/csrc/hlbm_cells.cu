@@ -72,7 +72,7 @@ __device__ __forceinline__ void add_moments(float m[10], int cx, int cy, int cz,
 // one link of the pull update; accumulates the raw moments of ft into m
 //   MODE 0: masked links take the half-way bounce-back population f+_opp(i)(x)
 //   MODE 2: masked links take the Eq.-8 boundary population at p = x - t c_i
-template <int I, bool Q16, bool FORCE, int MODE>
+template <int I, bool Q16, bool FORCE, int MODE, int Q>
 __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z, uint32_t mask,
                                           float m[10], MeshCtx& mc) {
   constexpr int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
@@ -86,7 +86,7 @@ __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z
   load_cell<Q16>(A, src_plane(g, sx), sy, sz, s);
   const Coef<float> C = coeffs<float, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
   float E, O;
-  eval_eo<cx, cy, cz, float>(C, E, O);
+  eval_eo<cx, cy, cz, float, Q>(C, E, O);
   float ft = bb ? (E - O) : (E + O);
   if (MODE == 2 && cut) {
     // Eq. 8: rho_p = rho_x, u_p = v + w x (p - c), rho S_p = rho u_p u_p + (rho S_x - rho u_x u_x)
@@ -115,16 +115,16 @@ __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z
   add_moments(m, cx, cy, cz, ft);
 }
 
-template <int I, bool Q16, bool FORCE, int MODE>
+template <int I, bool Q16, bool FORCE, int MODE, int Q>
 struct PullAll {
   __device__ __forceinline__ static void run(const StepArgs& A, int x, int y, int z, uint32_t mask,
                                              float m[10], MeshCtx& mc) {
-    pull_link<I, Q16, FORCE, MODE>(A, x, y, z, mask, m, mc);
-    PullAll<I + 1, Q16, FORCE, MODE>::run(A, x, y, z, mask, m, mc);
+    pull_link<I, Q16, FORCE, MODE, Q>(A, x, y, z, mask, m, mc);
+    PullAll<I + 1, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
   }
 };
-template <bool Q16, bool FORCE, int MODE>
-struct PullAll<27, Q16, FORCE, MODE> {
+template <bool Q16, bool FORCE, int MODE, int Q>
+struct PullAll<Q, Q16, FORCE, MODE, Q> {
   __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*, MeshCtx&) {}
 };
 
@@ -208,23 +208,25 @@ __device__ __forceinline__ void flush_stats(const StepArgs& A, float red[5]) {
 // MODE 3: the fused single-kernel step (Alg. 1, original HOME-LBM): every cell of the
 //         slab, one thread each, 27-link pull with the solid links resolved inline from a dense
 //         per-cell mask (bit 0: the cell is solid -> rest; bits 1..26: cut links -> bounce-back)
-template <bool Q16, bool FORCE, bool DITHER, int MODE>
+// Q: the velocity set, 27 or 19 (D3Q19 runs on this per-cell path only).  Without a cell list
+// the thread index is the local linear cell index offset by `base` (an x-range of the slab).
+template <bool Q16, bool FORCE, bool DITHER, int MODE, int Q>
 __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepArgs A,
                                                   const int64_t* __restrict__ cells,
-                                                  const uint32_t* __restrict__ masks, int64_t n) {
+                                                  const uint32_t* __restrict__ masks, int64_t n, int64_t base) {
   const Geo& g = A.g;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
   MeshCtx mc;
   mc.F[0] = mc.F[1] = mc.F[2] = mc.T[0] = mc.T[1] = mc.T[2] = 0.f;
   if (idx < n) {
-    const int64_t cell = cells ? cells[idx] : idx;
+    const int64_t cell = cells ? cells[idx] : base + idx;
     const int64_t yz = (int64_t)g.ny * g.nz;
     const int x = (int)(cell / yz);
     const int64_t r = cell - (int64_t)x * yz;
     const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
     float s[10];
-    const uint32_t fmask = (MODE == 3 && masks) ? masks[idx] : 0u;
+    const uint32_t fmask = (MODE == 3 && masks) ? masks[cell] : 0u;
     if (MODE == 1 || (MODE == 3 && (fmask & 1u))) {
 #pragma unroll
       for (int c = 0; c < 10; ++c) s[c] = 0.f;
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepAr
       float m[10];
 #pragma unroll
       for (int c = 0; c < 10; ++c) m[c] = 0.f;
-      PullAll<0, Q16, FORCE, MODE == 3 ? 0 : MODE>::run(A, x, y, z, mask, m, mc);
+      PullAll<0, Q16, FORCE, MODE == 3 ? 0 : MODE, Q>::run(A, x, y, z, mask, m, mc);
       raw_to_state<float>(m, s);
     }
     store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && MODE != 1 && !(MODE == 3 && (fmask & 1u)), red);
@@ -268,17 +270,22 @@ __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepAr
 
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither,
-                              cudaStream_t st) {
+                              cudaStream_t st, int q, int64_t base) {
   if (n <= 0) return cudaSuccess;
   const int tpb = 128;
   const int64_t nb = (n + tpb - 1) / tpb;
-#define HLBM_PULL(Q, F, D)                                                                      \
-  if (q16 == Q && force == F && dither == D) {                                                  \
-    if (mode == 0) pull_cells<Q, F, D, 0><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);   \
-    else if (mode == 1) pull_cells<Q, F, D, 1><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n); \
-    else if (mode == 2) pull_cells<Q, F, D, 2><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n); \
-    else pull_cells<Q, F, D, 3><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n);             \
-    return cudaGetLastError();                                                                  \
+#define HLBM_PULL(QQ, F, D)                                                                                    \
+  if (q16 == QQ && force == F && dither == D) {                                                              \
+    if (q == 19) {                                                                                           \
+      if (mode == 0) pull_cells<QQ, F, D, 0, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);      \
+      else if (mode == 1) pull_cells<QQ, F, D, 1, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
+      else if (mode == 3) pull_cells<QQ, F, D, 3, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
+      else return cudaErrorInvalidValue;                                                                     \
+    } else if (mode == 0) pull_cells<QQ, F, D, 0, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
+    else if (mode == 1) pull_cells<QQ, F, D, 1, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);   \
+    else if (mode == 2) pull_cells<QQ, F, D, 2, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);   \
+    else pull_cells<QQ, F, D, 3, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);                  \
+    return cudaGetLastError();                                                                               \
   }
   HLBM_PULL(false, false, false)
   HLBM_PULL(false, true, false)
@@ -317,7 +324,7 @@ __global__ void classify_cells(const uint8_t* __restrict__ mask_ext, MaskGeo m,
     if (!solid) {
 #pragma unroll
       for (int k = 1; k < 27; ++k)
-        if (padded_solid(mask_ext, m, x - kCX[k], y - kCY[k], z - kCZ[k])) lm |= 1u << k;
+        if (k < m.q && padded_solid(mask_ext, m, x - kCX[k], y - kCY[k], z - kCZ[k])) lm |= 1u << k;
     }
     links[i] = lm;
     cls[i] = (uint8_t)((lm != 0 ? 1 : 0) | (solid ? 2 : 0));

@@ -11,6 +11,7 @@ struct Ranges {
 struct MaskGeo {
   int nx, ny, nz;
   int bc_ywall_lo, bc_ywall_hi, bc_zwall_lo, bc_zwall_hi;
+  int q;   // velocity set (27 or 19): links counted
 };
 
 // qmode: 0 generic bit widths, 1 all 16-bit, 2 all 16-bit with the default QuantSpec ranges
@@ -34,7 +35,8 @@ cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool 
 // 2: triangle mesh, Eq.-8 boundary populations on masked links (t table in A.cut_t);
 // 3: fused single-kernel step over all cells with a dense per-cell mask (Alg. 1 baseline)
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
-                              int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st);
+                              int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st,
+                              int q = 27, int64_t base = 0);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
                           const double* mom, const double* stress, int x0, int cnt,
                           unsigned long long* sat, cudaStream_t st);

@@ -182,9 +182,11 @@ __device__ __forceinline__ Coef<T> coeffs(T d, T jx, T jy, T jz, T nxx, T nxy, T
 }
 
 // ft_i for one compile-time direction (cx,cy,cz) and sign s = +1 (c) or -1 (-c):
-// returns omega(c) * P(s c)  (= 216 w_i P(s c) / 216 -> exactly ft_i).  Even/odd split:
-// P(+-c) = E(c) +- O(c).
-template <int cx, int cy, int cz, class T>
+// returns 216 w_i P(s c) (= exactly ft_i = f_i - w_i).  D3Q27: 216 w_i = omega(cx) omega(cy)
+// omega(cz); D3Q19 (Q = 19, lattice.py:119-124): 216 w_i = 72 / 12 / 6 for |c|^2 = 0 / 1 / 2 -- the
+// xyz Hermite term vanishes on every D3Q19 velocity (moments.py:74-76), so P is the same
+// polynomial.  Even/odd split: P(+-c) = E(c) +- O(c).
+template <int cx, int cy, int cz, class T, int Q = 27>
 __device__ __forceinline__ void eval_eo(const Coef<T>& C, T& E, T& O) {
   // even part: K0 + Qaa c_a^2 + Qab c_a c_b
   T e = C.K0;
@@ -208,7 +210,9 @@ __device__ __forceinline__ void eval_eo(const Coef<T>& C, T& E, T& O) {
   if (cx && cz) { acc(cz, C.Txxz); acc(cx, C.Txzz); }
   if (cy && cz) { acc(cy, C.Tyzz); acc(cz, C.Tyyz); }
   if (cx && cy && cz) acc(cx * cy * cz, C.Txyz);
-  const float om = (cx ? 1.f : 4.f) * (cy ? 1.f : 4.f) * (cz ? 1.f : 4.f);
+  constexpr int c2 = cx * cx + cy * cy + cz * cz;
+  const float om = Q == 19 ? (c2 == 0 ? 72.f : (c2 == 1 ? 12.f : 6.f))
+                           : (cx ? 1.f : 4.f) * (cy ? 1.f : 4.f) * (cz ? 1.f : 4.f);
   if (om != 1.f) { e = vmul(e, splat<T>(om)); o = first ? o : vmul(o, splat<T>(om)); }
   E = e;
   O = o;

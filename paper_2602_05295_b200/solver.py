@@ -75,8 +75,8 @@ class SolverConfig:
     xseg: int = 0
 
     def __post_init__(self):
-        if self.lattice.upper() != "D3Q27":
-            raise ValueError("the B200 step implements the D3Q27 lattice")
+        if self.lattice.upper() not in ("D3Q27", "D3Q19"):
+            raise ValueError("the B200 step implements the D3Q27 and D3Q19 lattices")
         if self.precision not in _lib.PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(_lib.PRECISIONS)}")
         if not self.tau > 0.5:
@@ -165,6 +165,7 @@ class Solver:
         c.seed = int(config.seed) & 0xFFFFFFFF
         c.device = int(config.device)
         c.xseg = int(config.xseg)
+        c.q = 19 if config.lattice.upper() == "D3Q19" else 27   # D3Q19: per-cell fused kernel
         ctx = C.c_void_p()
         rc = self._lib.hlbm_create(C.byref(c), C.byref(ctx))
         self._ctx = ctx

@@ -11,6 +11,8 @@ outputs of the reference's own functions:
   step16.npz         one periodic step of a random 16^3 state composed from the reference
                      functions + np.roll pull streaming (SURVEY.md §8c golden vector 1)
   tgv32.npz          Taylor-Green 32^3 after 10 steps, same composition
+  d3q19.npz          make_lattice("D3Q19") tables and 1 / 3 periodic steps of a random
+                     12x14x16 state with the D3Q19 lattice, same composition
 """
 
 from __future__ import annotations
@@ -32,14 +34,27 @@ import momentlbm.lattice as RL  # noqa: E402
 import momentlbm.moments as RM  # noqa: E402
 
 LAT = RL.make_lattice("D3Q27")
+LAT19 = RL.make_lattice("D3Q19")
 
 
-def ref_step(rho, mom, stress, tau, force=None):
+def ref_step(rho, mom, stress, tau, force=None, lat=LAT):
     """Alg. 2 from the reference's own functions."""
     r, m, s = RC.collide_moments(rho, mom, stress, force, tau, 3)
-    f = RM.reconstruct_distributions(r, m, s, LAT)
-    fs = np.stack([np.roll(f[i], shift=tuple(LAT.velocities[i]), axis=(0, 1, 2)) for i in range(27)])
-    return RM.moments_from_distributions(fs, LAT)
+    f = RM.reconstruct_distributions(r, m, s, lat)
+    fs = np.stack([np.roll(f[i], shift=tuple(lat.velocities[i]), axis=(0, 1, 2)) for i in range(lat.q)])
+    return RM.moments_from_distributions(fs, lat)
+
+
+def write_d3q19():
+    h = LAT19.hermite
+    tau = 0.5 + 3 * 0.02
+    rho, mom, st = random_state((12, 14, 16), 3, 0.05, 0.08, 0.005)
+    s1 = ref_step(rho, mom, st, tau, lat=LAT19)
+    s3 = ref_step(*ref_step(*s1, tau, lat=LAT19), tau, lat=LAT19)
+    np.savez_compressed(HERE / "d3q19.npz", velocities=LAT19.velocities, weights=LAT19.weights,
+                        opposite=LAT19.opposite, h2c=h.h2_contract, h3=h.h3, tau=tau, rho=rho, mom=mom,
+                        stress=st, rho1=s1[0], mom1=s1[1], stress1=s1[2], rho3=s3[0], mom3=s3[1],
+                        stress3=s3[2])
 
 
 def random_state(shape, seed, drho, umax, sneq):
@@ -98,8 +113,12 @@ def main():
         r, m, s = ref_step(r, m, s, tau)
     np.savez_compressed(HERE / "tgv32.npz", tau=tau, steps=10, rho0=init[0], mom0=init[1],
                         stress0=init[2], rho=r, mom=m, stress=s)
+    write_d3q19()
     print("golden fixtures written to", HERE)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--d3q19"]:
+        write_d3q19()
+    else:
+        main()

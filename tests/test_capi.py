@@ -87,3 +87,9 @@ def test_invalid_grid_rejected_by_the_library():
     assert lib.hlbm_create(C.byref(c), C.byref(ctx)) == _lib.HLBM_EINVAL
     assert b"tau" in lib.hlbm_last_error(ctx)
     lib.hlbm_destroy(ctx)
+
+
+def test_lattice_choice_validation():
+    assert SolverConfig(lattice="D3Q19").lattice == "D3Q19"
+    with pytest.raises(ValueError):
+        SolverConfig(lattice="D3Q15")

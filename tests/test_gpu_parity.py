@@ -274,3 +274,54 @@ def test_fused_alg1_q16_matches_split_within_1_lsb():
             words[scheme] = s.codes
     d = np.abs(codec.unpack(words["fused"]).astype(np.int64) - codec.unpack(words["split"]).astype(np.int64))
     assert d.max() <= 1
+
+
+# ------------------------------------------------------------------------------------ D3Q19
+def test_d3q19_matches_reference_golden():
+    """D3Q19 (per-cell fused kernel) against the reference's own D3Q19 composition."""
+    z = np.load(G / "d3q19.npz")
+    cfg = SolverConfig(nu=(float(z["tau"]) - 0.5) / 3, lattice="D3Q19")
+    for steps, key in ((1, "1"), (3, "3")):
+        got = run_gpu((z["rho"], z["mom"], z["stress"]), cfg, steps)
+        err = moment_errors(got, (z["rho" + key], z["mom" + key], z["stress" + key]))
+        assert max(err) <= FP32_TOL, (steps, err)
+
+
+@pytest.mark.parametrize("bcname", ["channel", "closed"])
+def test_d3q19_solids_and_bcs(bcname):
+    from oracle import lattice as OL
+    shape = (24, 20, 28)
+    mask = sphere_mask(shape, (10, 9.5, 13.5), 4)
+    if bcname == "channel":
+        bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("wall", "wall")}
+    else:
+        bc = {"x": ("wall", "wall"), "y": ("wall", "wall"), "z": ("wall", "wall")}
+    cfg = SolverConfig(nu=0.02, bc=bc, u_in=(0.05, 0, 0), lattice="D3Q19")
+    obc = OS.BC(x=bc["x"], y=bc["y"], z=bc["z"], u_in=(0.05, 0, 0))
+    cells, masks = OS.boundary_lists(mask, obc, OL.D3Q19)
+    state = _channel_state(shape, mask, 0.05)
+    with Solver(SimGrid(shape, mask), cfg) as s:
+        gc, gm = s.boundary()
+        assert np.array_equal(gc, cells) and np.array_equal(gm, masks)   # 19-link masks, bit-exact
+        s.set_moments(*state)
+        st = s.step(4)
+        got = s.moments()
+    ref = OS.run(*state, cfg.tau, 4, obc, None, mask, OL.D3Q19)
+    fl = ~mask.astype(bool)
+    assert max(moment_errors(got, ref, fl)) <= FP32_TOL
+    assert st.mass == pytest.approx(ref[0][fl].sum(), rel=1e-7)
+
+
+def test_d3q19_q16_within_1_lsb():
+    from oracle import lattice as OL
+    shape = (12, 16, 20)
+    state = OS.random_state(shape, seed=4, drho=0.05, umax=0.05, sneq=0.005)
+    cfg = SolverConfig(nu=0.02, precision="q16", quant=QuantSpec(), lattice="D3Q19")
+    words0, _ = codec.encode_state(state[0], state[1], neq_decompose(*state))
+    with Solver(SimGrid(shape), cfg) as s:
+        s.codes = words0
+        s.step(1)
+        words = s.codes
+    ref, _ = OS.fluid_step_q16(words0, cfg.tau, 0, lat=OL.D3Q19)
+    d = np.abs(codec.unpack(words).astype(np.int64) - codec.unpack(ref).astype(np.int64))
+    assert d.max() <= 1

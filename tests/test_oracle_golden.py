@@ -73,3 +73,21 @@ def test_tgv32_ten_steps_against_reference_composition():
     r0, m0, s0 = OS.taylor_green(32)
     np.testing.assert_allclose(r0, z["rho0"], rtol=0, atol=1e-15)
     np.testing.assert_allclose(m0, z["mom0"], rtol=0, atol=1e-15)
+
+
+def test_oracle_d3q19_matches_reference():
+    """D3Q19 lattice tables and 1 / 3 periodic steps (reference composition, tests/golden/d3q19.npz)."""
+    z = np.load(G / "d3q19.npz")
+    lat = OL.D3Q19
+    assert np.array_equal(lat.C, z["velocities"])
+    np.testing.assert_array_equal(lat.W, z["weights"])
+    assert np.array_equal(lat.OPP, z["opposite"])
+    np.testing.assert_allclose(lat.H2C, z["h2c"], rtol=0, atol=0)
+    np.testing.assert_allclose(lat.H3, z["h3"], rtol=0, atol=1e-15)
+    tau = float(z["tau"])
+    got1 = OS.run(z["rho"], z["mom"], z["stress"], tau, 1, lat=lat)
+    got3 = OS.run(z["rho"], z["mom"], z["stress"], tau, 3, lat=lat)
+    for g, r in zip(got1, (z["rho1"], z["mom1"], z["stress1"])):
+        np.testing.assert_allclose(g, r, rtol=0, atol=1e-15)
+    for g, r in zip(got3, (z["rho3"], z["mom3"], z["stress3"])):
+        np.testing.assert_allclose(g, r, rtol=0, atol=1e-14)
