@@ -197,6 +197,15 @@ int plane_offsets(hlbm_ctx* ctx, const int64_t* d_cells, int64_t n, std::vector<
   return HLBM_OK;
 }
 
+// a one-row slab (ny == 1): the interior kernel writes only the y = ny ghost image of an edge row;
+// refresh both ghost rows of the written buffer (tiny grids only, off the hot kernel)
+int fix_one_row(hlbm_ctx* ctx) {
+  if (ctx->cfg.ny != 1) return HLBM_OK;
+  CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], ctx->stream));
+  ++ctx->launches;
+  return HLBM_OK;
+}
+
 // interior kernel + compacted boundary kernels for destination planes [xb, xr)
 int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_interior = nullptr) {
   if (xr <= xb) return HLBM_OK;
@@ -210,7 +219,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
                          (int64_t)xb * pl));
     ++ctx->launches;
     if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
-    return HLBM_OK;
+    return fix_one_row(ctx);
   }
   CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
   ++ctx->launches;
@@ -238,7 +247,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
     CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, ctx->stream));
     ++ctx->launches;
   }
-  return HLBM_OK;
+  return fix_one_row(ctx);
 }
 
 }  // namespace

@@ -10,6 +10,8 @@
 //   classify / compact   voxel mask -> sorted boundary-cell list + 27-bit link masks and the
 //                   solid list, deterministic (block prefix sums, no atomics in the ordering).
 //   import / export reference layout (rho, mom, stress float64) <-> internal state.
+#include <climits>
+
 #include "hlbm_launch.h"
 
 namespace hlbm {
@@ -130,13 +132,14 @@ struct PullAll<Q, Q16, FORCE, MODE, Q> {
 
 template <typename E>
 __device__ __forceinline__ void put_cell(const Geo& g, E* plane, int y, int z, const E* v, int ncomp) {
-  // the cell and, at y/z edges, its periodic images in the ghost layers
-  const int yi = y == 0 ? g.ny : (y == g.ny - 1 ? -1 : y);
-  const int zi = z == 0 ? g.nz : (z == g.nz - 1 ? -1 : z);
-  for (int a = 0; a < 2; ++a)
-    for (int b = 0; b < 2; ++b) {
-      if ((a && yi == y) || (b && zi == z)) continue;
-      E* p = plane + (int64_t)((a ? yi : y) + 1) * g.zp + ((b ? zi : z) + kZOff);
+  // the cell and, at y/z edges, its periodic images in the ghost layers (both y ghost rows
+  // when ny == 1, both z ghost columns when nz == 1)
+  const int ys[3] = {y, y == 0 ? g.ny : INT_MIN, y == g.ny - 1 ? -1 : INT_MIN};
+  const int zs[3] = {z, z == 0 ? g.nz : INT_MIN, z == g.nz - 1 ? -1 : INT_MIN};
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      if (ys[a] == INT_MIN || zs[b] == INT_MIN) continue;
+      E* p = plane + (int64_t)(ys[a] + 1) * g.zp + (zs[b] + kZOff);
       for (int c = 0; c < ncomp; ++c) p[c * g.cstride] = v[c];
     }
 }

@@ -44,6 +44,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef HLBM_WAIT_HINT_NS   // optional suspend-time hint (ns) for the blocking try_wait
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HLBM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra HLBM_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(HLBM_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "HLBM_WAIT_%=:\n"
@@ -51,6 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       " @!p bra HLBM_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             int c3, uint64_t* bar) {
