@@ -37,6 +37,8 @@ struct hlbm_ctx {
   Codec Q{};
   Ranges RG{};
   float inflow[10] = {};
+  double om_d = 0.0;                          // 1 - s in double (coeffs_pre input scales)
+  double dec_step_d[10] = {}, dec_off_d[10] = {};
   int x_lo_src = 0, x_hi_src = 0;
   // solids
   int64_t* d_bcells = nullptr;
@@ -126,7 +128,14 @@ StepArgs make_args(hlbm_ctx* ctx, int with_stats, int xb = 0, int xr = -1) {
   A.g = make_geo(ctx, xb, xr);
   A.R = ctx->R;
   A.Q = ctx->Q;
-  for (int i = 0; i < 10; ++i) A.inflow[i] = ctx->inflow[i];
+  for (int i = 0; i < 10; ++i) {
+    A.inflow[i] = ctx->inflow[i];
+    const double k = pre_scale(i, ctx->om_d);
+    A.pre_step[i] = (float)(ctx->dec_step_d[i] * k);
+    A.pre_off[i] = (float)(ctx->dec_off_d[i] * k);
+    A.pre_k[i] = (float)k;
+    A.inflow_pre[i] = (float)((double)ctx->inflow[i] * k);
+  }
   A.special_bits = ctx->d_bits;
   A.bits_row_words = ctx->bits_row_words;
   A.step_key = step_key(ctx->steps, ctx->cfg.seed);
@@ -316,6 +325,7 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
   // relaxation constants (collision.py:158-191)
   const double tau = c.tau, s = 1.0 / tau;
   ctx->R.om = (float)(1.0 - s);
+  ctx->om_d = 1.0 - s;
   ctx->R.cxy = (float)((2 * tau - 1) / (2 * tau));
   ctx->R.cd = (float)((tau - 1) / (3 * tau));
   ctx->R.fx = (float)c.force[0];
@@ -336,6 +346,8 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
     const double shift = (k == 0) ? 1.0 : 0.0;   // component 0 is held as d = rho - 1
     ctx->Q.dec_step[k] = (float)((mx - mn) / L);
     ctx->Q.dec_off[k] = (float)(mn - shift);
+    ctx->dec_step_d[k] = (mx - mn) / L;
+    ctx->dec_off_d[k] = mn - shift;
     const double sc = L / (mx - mn);
     ctx->Q.enc_scale[k] = (float)sc;
     ctx->Q.enc_off[k] = (float)((shift - mn) * sc + 0.5);

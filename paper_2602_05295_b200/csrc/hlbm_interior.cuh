@@ -280,17 +280,32 @@ template <int QMODE> __device__ __forceinline__ float q_enc_off(const Codec& Q, 
   return QMODE == 2 ? DefQ::enc_off(c) : Q.enc_off[c];
 }
 
-template <bool Q16, int QMODE>
+// PRE: the values come out in the coeffs_pre input scales (hlbm_math.cuh) -- folded into the
+// decode FMA for 16-bit codes, one multiply per component for fp32
+template <bool Q16, int QMODE, bool PRE>
 __device__ __forceinline__ void load_state(const uint32_t (*st)[kBoxRows][kZW], int row, int lane,
                                            bool inflow, const StepArgs& A, V s[10]) {
   if (inflow) {
 #pragma unroll
-    for (int c = 0; c < 10; ++c) s[c] = vsplat(A.inflow[c]);
+    for (int c = 0; c < 10; ++c) s[c] = vsplat(PRE ? A.inflow_pre[c] : A.inflow[c]);
     return;
   }
   if (!Q16) {
 #pragma unroll
-    for (int c = 0; c < 10; ++c) s[c] = *reinterpret_cast<const V*>(&st[c][row][2 * lane]);
+    for (int c = 0; c < 10; ++c) {
+      s[c] = *reinterpret_cast<const V*>(&st[c][row][2 * lane]);
+      if (PRE) s[c] = vmul(s[c], A.pre_k[c]);
+    }
+  } else if (PRE) {
+    const V two23 = vsplat(8388608.0f);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint2 wv = *reinterpret_cast<const uint2*>(&st[k][row][2 * lane]);
+      const V lo = make_float2(code_lo_f(wv.x), code_lo_f(wv.y));
+      const V hi = make_float2(code_hi_f(wv.x), code_hi_f(wv.y));
+      s[2 * k] = vfma(vsub(lo, two23), vsplat(A.pre_step[2 * k]), vsplat(A.pre_off[2 * k]));
+      s[2 * k + 1] = vfma(vsub(hi, two23), vsplat(A.pre_step[2 * k + 1]), vsplat(A.pre_off[2 * k + 1]));
+    }
   } else {
     const V two23 = vsplat(8388608.0f);
 #pragma unroll
@@ -304,6 +319,15 @@ __device__ __forceinline__ void load_state(const uint32_t (*st)[kBoxRows][kZW], 
                           vsplat(q_dec_off<QMODE>(A.Q, 2 * k + 1)));
     }
   }
+}
+
+// reconstruction coefficients of a loaded cell pair (load_state<.., PRE = !FORCE> scales)
+template <bool FORCE>
+__device__ __forceinline__ Coef<V> coeffs_int(const V s[10], const Relax& R) {
+  if constexpr (FORCE)
+    return coeffs<V, true>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], R);
+  else
+    return coeffs_pre<V>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9]);
 }
 
 // a finished cell pair (z even, z+1) of row y: `cell` points at component 0 of the pair in its
@@ -515,15 +539,15 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       mbar_wait(&S.empty[b][xrow], eph ^ 1u);
       if (do_lo) {
         V s[10];
-        load_state<Q16, QMODE>(S.stage[st], 0, lane, inflow, A, s);
-        const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+        load_state<Q16, QMODE, !FORCE>(S.stage[st], 0, lane, inflow, A, s);
+        const Coef<V> C = coeffs_int<FORCE>(s, A.R);
         if (!do_hi) consumed();
         recon_halo<0>(C, S.exch[b], 0, lane);
       }
       if (do_hi) {
         V s[10];
-        load_state<Q16, QMODE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
-        const Coef<V> C = coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+        load_state<Q16, QMODE, !FORCE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
+        const Coef<V> C = coeffs_int<FORCE>(s, A.R);
         consumed();
         recon_halo<1>(C, S.exch[b], xrow, lane);
       }
@@ -557,9 +581,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       V zcen[3][3];  // [kx][az]: ky = 0 z-stage values of this source row (y centre term)
       {
         V s[10];
-        load_state<Q16, QMODE>(S.stage[st], w, lane, plane_inflow(p), A, s);
-        const Coef<V> C =
-            coeffs<V, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+        load_state<Q16, QMODE, !FORCE>(S.stage[st], w, lane, plane_inflow(p), A, s);
+        const Coef<V> C = coeffs_int<FORCE>(s, A.R);
         consumed();   // C depends on every loaded value
         // my slots of buffer b were read by my neighbours NB planes ago
         mbar_wait(&S.empty[b][w], eph ^ 1u);

@@ -116,6 +116,58 @@ __device__ __forceinline__ Coef<T> hermite(T d, T jpx, T jpy, T jpz, T ux, T uy,
 }
 
 
+// Collision + Hermite expansion from PRE-SCALED stored moments (no body force; the hot path).
+// The constants of the expansion are folded into the inputs, which the kernels obtain for free
+// (the 16-bit decode FMA or one multiply per component):
+//   dt = d/216,  jt = j/72,  naa = (4.5/216)(1-s) sneq_aa,  nab = (9/216)(1-s) sneq_ab.
+// With u3 = 3u = jt * 216/rho and p_a = jt_a u3_a (= j_a u_a / 24), the coeffs() algebra becomes
+//   R_aa = naa - tr(n)/3                       (the relaxed deviatoric stress, x q2)
+//   Q_aa = R_aa + p_a/2,  Q_ab = jt_a u3_b + nab      (X = (1-s) sneq + j u, x q2 / q11)
+//   al'_a = R_aa - p_a/2                       (al_a / 3, collision.py:176-191 via coeffs())
+//   T_aab = al'_a u3_b + Q_ab u3_a,  T_xyz = (Q_xy u3z + Q_xz u3y + Q_yz u3x)/2 - jt_x u3y u3z
+//   K0 = dt - (p_x + p_y + p_z)/6,  L_a = jt_a - (T_abb + T_acc)/3
+// (K0 uses tr R = 0; the rest is the same polynomial as coeffs(), moments.py:64-90): 48 instead
+// of 69 packed FP operations per cell pair.
+template <class T>
+__device__ __forceinline__ Coef<T> coeffs_pre(T dt, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy,
+                                              T nyz, T nzz) {
+  const T inv = vrcp(vadd(dt, splat<T>(1.0f / 216.0f)));   // 216 / rho
+  const T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);   // 3 u
+  const T tr = vadd(vadd(nxx, nyy), nzz);
+  const T third = splat<T>(-1.0f / 3.0f), half = splat<T>(0.5f), mhalf = splat<T>(-0.5f);
+  const T Rxx = vfma(tr, third, nxx), Ryy = vfma(tr, third, nyy), Rzz = vfma(tr, third, nzz);
+  const T px = vmul(jx, ux), py = vmul(jy, uy), pz = vmul(jz, uz);
+  Coef<T> C;
+  C.Qxx = vfma(px, half, Rxx);
+  C.Qyy = vfma(py, half, Ryy);
+  C.Qzz = vfma(pz, half, Rzz);
+  const T alx = vfma(px, mhalf, Rxx), aly = vfma(py, mhalf, Ryy), alz = vfma(pz, mhalf, Rzz);
+  C.Qxy = vfma(jx, uy, nxy);
+  C.Qxz = vfma(jx, uz, nxz);
+  C.Qyz = vfma(jy, uz, nyz);
+  C.Txxy = vfma(alx, uy, vmul(C.Qxy, ux));
+  C.Txyy = vfma(aly, ux, vmul(C.Qxy, uy));
+  C.Txxz = vfma(alx, uz, vmul(C.Qxz, ux));
+  C.Txzz = vfma(alz, ux, vmul(C.Qxz, uz));
+  C.Tyzz = vfma(alz, uy, vmul(C.Qyz, uz));
+  C.Tyyz = vfma(aly, uz, vmul(C.Qyz, uy));
+  const T A3 = vfma(C.Qxy, uz, vfma(C.Qxz, uy, vmul(C.Qyz, ux)));
+  C.Txyz = vfma(A3, half, vmul(vneg(vmul(jx, uy)), uz));
+  C.K0 = vfma(vadd(vadd(px, py), pz), splat<T>(-1.0f / 6.0f), dt);
+  C.Lx = vfma(vadd(C.Txyy, C.Txzz), third, jx);
+  C.Ly = vfma(vadd(C.Txxy, C.Tyzz), third, jy);
+  C.Lz = vfma(vadd(C.Txxz, C.Tyyz), third, jz);
+  return C;
+}
+
+// input scales of coeffs_pre (component order d, j, sneq Voigt xx,xy,xz,yy,yz,zz); om = 1 - s
+__host__ __device__ inline double pre_scale(int c, double om) {
+  if (c == 0) return 1.0 / 216.0;
+  if (c < 4) return 1.0 / 72.0;
+  const bool diag = (c == 4 || c == 7 || c == 9);
+  return (diag ? 4.5 / 216.0 : 9.0 / 216.0) * om;
+}
+
 // post-collision moments of one (pair of) cell(s): d = rho - 1, jp = rho u+ (mom + F/2),
 // u = u+, X = rho S+ (full stress)
 template <class T>

@@ -59,6 +59,9 @@ struct StepArgs {
   Relax R;
   Codec Q;
   float inflow[10];                 // internal-form state of an inflow ghost plane
+  float pre_step[10], pre_off[10];  // q16 decode straight into the coeffs_pre input scales
+  float pre_k[10];                  // fp32: input scales of coeffs_pre (hlbm_math.cuh pre_scale)
+  float inflow_pre[10];             // inflow ghost state in coeffs_pre scales
   const uint32_t* special_bits;     // per (xs,y) row bitmask of boundary/solid cells, or null
   int bits_row_words;               // u32 words per bitmask row
   uint32_t step_key;                // dither key for this step
