@@ -322,12 +322,12 @@ __device__ __forceinline__ void load_state(const uint32_t (*st)[kBoxRows][kZW], 
 }
 
 // reconstruction coefficients of a loaded cell pair (load_state<.., PRE = !FORCE> scales)
-template <bool FORCE>
+template <bool FORCE, bool Q16>
 __device__ __forceinline__ Coef<V> coeffs_int(const V s[10], const Relax& R) {
   if constexpr (FORCE)
     return coeffs<V, true>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], R);
   else
-    return coeffs_pre<V>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9]);
+    return coeffs_pre<V, Q16>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9]);
 }
 
 // a finished cell pair (z even, z+1) of row y: `cell` points at component 0 of the pair in its
@@ -360,7 +360,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
                                            bool staty, float* acc) {
   const Geo& g = A.g;
   V s[10], inv;
-  raw_to_state(m, s, &inv);
+  raw_to_state<V, Q16>(m, s, &inv);
   const int64_t plane_off = (int64_t)(q + 1) * g.pstride;
   const int64_t cell_off = plane_off + cell_off0;
   constexpr bool B16 = QMODE >= 1;
@@ -540,14 +540,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       if (do_lo) {
         V s[10];
         load_state<Q16, QMODE, !FORCE>(S.stage[st], 0, lane, inflow, A, s);
-        const Coef<V> C = coeffs_int<FORCE>(s, A.R);
+        const Coef<V> C = coeffs_int<FORCE, Q16>(s, A.R);
         if (!do_hi) consumed();
         recon_halo<0>(C, S.exch[b], 0, lane);
       }
       if (do_hi) {
         V s[10];
         load_state<Q16, QMODE, !FORCE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
-        const Coef<V> C = coeffs_int<FORCE>(s, A.R);
+        const Coef<V> C = coeffs_int<FORCE, Q16>(s, A.R);
         consumed();
         recon_halo<1>(C, S.exch[b], xrow, lane);
       }
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       {
         V s[10];
         load_state<Q16, QMODE, !FORCE>(S.stage[st], w, lane, plane_inflow(p), A, s);
-        const Coef<V> C = coeffs_int<FORCE>(s, A.R);
+        const Coef<V> C = coeffs_int<FORCE, Q16>(s, A.R);
         consumed();   // C depends on every loaded value
         // my slots of buffer b were read by my neighbours NB planes ago
         mbar_wait(&S.empty[b][w], eph ^ 1u);

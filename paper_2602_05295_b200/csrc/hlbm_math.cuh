@@ -54,6 +54,13 @@ __device__ __forceinline__ float rcp_nr(float x) {
 }
 __device__ __forceinline__ V vrcp(V x) { return make_float2(rcp_nr(x.x), rcp_nr(x.y)); }
 __device__ __forceinline__ float vrcp(float x) { return rcp_nr(x); }
+// MUFU.RCP alone (~1 ulp): used by the 16-bit paths, whose codes resolve ~1e-5 of a range
+__device__ __forceinline__ V vrcp_fast(V x) { return make_float2(rcp_approx(x.x), rcp_approx(x.y)); }
+__device__ __forceinline__ float vrcp_fast(float x) { return rcp_approx(x); }
+template <bool FAST, class T> __device__ __forceinline__ T vrcp_t(T x) {
+  if constexpr (FAST) return vrcp_fast(x);
+  else return vrcp(x);
+}
 
 // ------------------------------------------------------------------ relaxation constants
 struct Relax {
@@ -128,10 +135,10 @@ __device__ __forceinline__ Coef<T> hermite(T d, T jpx, T jpy, T jpz, T ux, T uy,
 //   K0 = dt - (p_x + p_y + p_z)/6,  L_a = jt_a - (T_abb + T_acc)/3
 // (K0 uses tr R = 0; the rest is the same polynomial as coeffs(), moments.py:64-90): 48 instead
 // of 69 packed FP operations per cell pair.
-template <class T>
+template <class T, bool FAST = false>
 __device__ __forceinline__ Coef<T> coeffs_pre(T dt, T jx, T jy, T jz, T nxx, T nxy, T nxz, T nyy,
                                               T nyz, T nzz) {
-  const T inv = vrcp(vadd(dt, splat<T>(1.0f / 216.0f)));   // 216 / rho
+  const T inv = vrcp_t<FAST>(vadd(dt, splat<T>(1.0f / 216.0f)));   // 216 / rho
   const T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);   // 3 u
   const T tr = vadd(vadd(nxx, nyy), nzz);
   const T third = splat<T>(-1.0f / 3.0f), half = splat<T>(0.5f), mhalf = splat<T>(-0.5f);
@@ -271,13 +278,12 @@ __device__ __forceinline__ void eval_eo(const Coef<T>& C, T& E, T& O) {
 }
 
 // raw moments (of ft) -> stored state: d = m0, j = m1, n = (Pi~ - delta d/3) - j j / rho
-template <class T>
+template <class T, bool FAST = false>
 __device__ __forceinline__ void raw_to_state(const T m[10], T out[10], T* inv_out = nullptr) {
   // m: [m000, m100, m010, m001, m200, m110, m101, m020, m011, m002]
   T d = m[0];
-  T inv = vrcp(vadd(d, splat<T>(1.0f)));
+  T inv = vrcp_t<FAST>(vadd(d, splat<T>(1.0f)));
   if (inv_out) *inv_out = inv;
-  T d3 = vmul(d, splat<T>(1.0f / 3.0f));
   T jx = m[1], jy = m[2], jz = m[3];
   T ux = vmul(jx, inv), uy = vmul(jy, inv), uz = vmul(jz, inv);
   out[0] = d;
@@ -286,12 +292,13 @@ __device__ __forceinline__ void raw_to_state(const T m[10], T out[10], T* inv_ou
   out[3] = jz;
   // sneq = Pi - d/3 delta - j u, the j u products fused into the subtraction (one rounding)
   const T njx = vneg(jx), njy = vneg(jy), njz = vneg(jz);
-  out[4] = vfma(njx, ux, vsub(m[4], d3));
+  const T m3 = splat<T>(-1.0f / 3.0f);
+  out[4] = vfma(njx, ux, vfma(d, m3, m[4]));
   out[5] = vfma(njx, uy, m[5]);
   out[6] = vfma(njx, uz, m[6]);
-  out[7] = vfma(njy, uy, vsub(m[7], d3));
+  out[7] = vfma(njy, uy, vfma(d, m3, m[7]));
   out[8] = vfma(njy, uz, m[8]);
-  out[9] = vfma(njz, uz, vsub(m[9], d3));
+  out[9] = vfma(njz, uz, vfma(d, m3, m[9]));
 }
 
 // ------------------------------------------------------------------ 16-bit codec
