@@ -221,8 +221,16 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   StepArgs A = make_args(ctx, with_stats, xb, xr);
+  if (ctx->q == 19 && !special && (!q16 || ctx->qmode == 2)) {
+    // D3Q19 fluid-only: the interior kernel with two-chain streaming (no boundary lists)
+    CK(launch_fluid_interior19(A, q16, force, dither, ctx->stream));
+    ++ctx->launches;
+    if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
+    return fix_one_row(ctx);
+  }
   if (ctx->q == 19) {
-    // D3Q19: the per-cell fused kernel over the planes of the range, solid links inline
+    // D3Q19 with solids or a non-default codec: the per-cell fused kernel over the planes of the
+    // range, solid links inline
     const int64_t pl = (int64_t)ctx->cfg.ny * ctx->cfg.nz;
     CK(launch_pull_cells(A, nullptr, ctx->d_fused, (int64_t)(xr - xb) * pl, 3, q16, force, dither, ctx->stream, 19,
                          (int64_t)xb * pl));

@@ -72,10 +72,10 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 }
 
 
-template <int NC, int STAGES, int NB>
+template <int NC, int STAGES, int NB, int NS = kNSlot>
 struct Smem {
   uint32_t stage[STAGES][NC][kBoxRows][kZW];
-  V exch[NB][kNSlot][kNW][32];  // y exchange (NB buffers); "row" 0 = halo warp (see ystage)
+  V exch[NB][NS][kNW][32];      // y exchange (NB buffers); "row" 0 = halo warp (see ystage)
   uint64_t bar[STAGES];         // TMA stage full (1 arrival + tx bytes)
   uint64_t full[NB][kNW];       // warp w's exchange slots of buffer b written (32 lane arrivals)
   uint64_t empty[NB][kNW];      // ... consumed by every y-stage neighbour of w (32 per reader)
@@ -123,6 +123,16 @@ struct Part6 {
 // exchange slot of (kx, s, az): s = 0 sent to row y+1 (Yp), s = 1 sent to row y-1 (Ym)
 __device__ __forceinline__ constexpr int xslot(int kx, int s, int az) { return (kx * 2 + s) * 3 + az; }
 
+// D3Q19 (LAT = 19): 216 w = prod_axis(4, 1, 1) + prod_axis(2, -1, -1) over (c = 0, +-1) -- rest
+// 64 + 8 = 72, axis 16 - 4 = 12, face 4 + 2 = 6, corner 1 - 1 = 0 (lattice.py:119-124) -- so the
+// step is the D3Q27 chain A plus a chain B with the 1-D weights (2, -1, -1).  Along an axis,
+// chain B's output is 2 F0 [a == 0] minus chain A's neighbour sums, so after the z stage chain B
+// equals -chain A for az >= 1 and differs only in its az = 0 fields, zB = 2 F0 - S = 6 F0 - z0.
+// The exchange carries chain B's az = 0 y sums in 6 extra slots; the chains merge in the x stage,
+// whose neighbour sums take W = Y_A - Y_B and whose centre term takes 4 Y_A + 2 Y_B.
+__device__ __forceinline__ constexpr int xslotB(int kx, int s) { return 18 + kx * 2 + s; }
+template <int LAT> struct LatSlots { static constexpr int n = LAT == 19 ? 24 : kNSlot; };
+
 // z pull of one (kx,ky) group from its inputs F0 (kz=0), F1 (kz=1), F2 (kz=2); N inputs present
 template <int N>
 __device__ __forceinline__ void zgroup(V F0, V F1, V F2, V z[3]) {
@@ -147,22 +157,39 @@ __device__ __forceinline__ void zgroup(V F0, V F1, V F2, V z[3]) {
   z[0] = vfma(F0, vsplat(4.0f), S);
   z[2] = S;
 }
+// chain B (D3Q19) az = 0 value of a group from its chain-A z0 and kz = 0 input
+__device__ __forceinline__ V zchainB(V F0, V z0) { return vfma(F0, vsplat(6.0f), vneg(z0)); }
 
-// z-stage of the groups with a given kx: Z[ky][az]
-template <int KX>
-__device__ __forceinline__ void zstage(const Coef<V>& C, V Z[3][3]) {
+// z-stage of the groups with a given kx: Z[ky][az]; LAT 19 also ZB[ky] (chain B, az = 0)
+template <int KX, int LAT = 27>
+__device__ __forceinline__ void zstage(const Coef<V>& C, V Z[3][3], V* ZB = nullptr) {
   const V o = vsplat(0.f);
   if (KX == 0) {
     zgroup<3>(C.K0, C.Lz, C.Qzz, Z[0]);
     zgroup<3>(C.Ly, C.Qyz, C.Tyzz, Z[1]);
     zgroup<2>(C.Qyy, C.Tyyz, o, Z[2]);
+    if (LAT == 19) { ZB[0] = zchainB(C.K0, Z[0][0]); ZB[1] = zchainB(C.Ly, Z[1][0]); ZB[2] = zchainB(C.Qyy, Z[2][0]); }
   } else if (KX == 1) {
     zgroup<3>(C.Lx, C.Qxz, C.Txzz, Z[0]);
     zgroup<2>(C.Qxy, C.Txyz, o, Z[1]);
     zgroup<1>(C.Txyy, o, o, Z[2]);
+    if (LAT == 19) { ZB[0] = zchainB(C.Lx, Z[0][0]); ZB[1] = zchainB(C.Qxy, Z[1][0]); ZB[2] = zchainB(C.Txyy, Z[2][0]); }
   } else {
     zgroup<2>(C.Qxx, C.Txxz, o, Z[0]);
     zgroup<1>(C.Txxy, o, o, Z[1]);
+    if (LAT == 19) { ZB[0] = zchainB(C.Qxx, Z[0][0]); ZB[1] = zchainB(C.Txxy, Z[1][0]); }
+  }
+}
+// chain-B y sums of (kx, az = 0)
+template <int KX>
+__device__ __forceinline__ void ysumsB(const V ZB[3], V& Yp, V& Ym) {
+  if (KX < 2) {
+    const V P = vadd(ZB[0], ZB[2]);
+    Yp = vadd(P, ZB[1]);
+    Ym = vsub(P, ZB[1]);
+  } else {
+    Yp = vadd(ZB[0], ZB[1]);
+    Ym = vsub(ZB[0], ZB[1]);
   }
 }
 
@@ -179,11 +206,20 @@ __device__ __forceinline__ void ysums(const V Z[3][3], int az, V& Yp, V& Ym) {
   }
 }
 
-// own row, one kx: both y sums to the exchange, the ky = 0 centre values returned
-template <int KX>
-__device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane, V zc[3]) {
-  V Z[3][3];
-  zstage<KX>(C, Z);
+// own row, one kx: both y sums to the exchange, the ky = 0 centre values returned (LAT 19: and
+// chain B's az = 0 centre value in *zcb)
+template <int KX, int LAT = 27>
+__device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], int w, int lane, V zc[3],
+                                          V* zcb = nullptr) {
+  V Z[3][3], ZB[3];
+  zstage<KX, LAT>(C, Z, ZB);
+  if constexpr (LAT == 19) {
+    V p, m;
+    ysumsB<KX>(ZB, p, m);
+    exch[xslotB(KX, 0)][w][lane] = p;
+    exch[xslotB(KX, 1)][w][lane] = m;
+    *zcb = ZB[0];
+  }
 #pragma unroll
   for (int az = 0; az < 3; ++az) {
     V p, m;
@@ -196,16 +232,21 @@ __device__ __forceinline__ void recon_row(const Coef<V>& C, V (*exch)[kNW][32], 
 
 // halo row: only the y sum that enters the tile (S = 0: row y0-1 sends Yp up; S = 1: row
 // y0+15 sends Ym down), into the exchange slots of "row" 0
-template <int S>
+template <int S, int LAT = 27>
 __device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32], int xrow, int lane) {
 #define HLBM_HALO_KX(KX)                                  \
   {                                                       \
-    V Z[3][3];                                            \
-    zstage<KX>(C, Z);                                     \
+    V Z[3][3], ZB[3];                                     \
+    zstage<KX, LAT>(C, Z, ZB);                            \
     _Pragma("unroll") for (int az = 0; az < 3; ++az) {    \
       V p, m;                                             \
       ysums<KX>(Z, az, p, m);                             \
       exch[xslot(KX, S, az)][xrow][lane] = S == 0 ? p : m; \
+    }                                                     \
+    if constexpr (LAT == 19) {                            \
+      V p, m;                                             \
+      ysumsB<KX>(ZB, p, m);                               \
+      exch[xslotB(KX, S)][xrow][lane] = S == 0 ? p : m;   \
     }                                                     \
   }
   HLBM_HALO_KX(0) HLBM_HALO_KX(1) HLBM_HALO_KX(2)
@@ -221,25 +262,61 @@ __device__ __forceinline__ void recon_halo(const Coef<V>& C, V (*exch)[kNW][32],
 //                   each Nq entry is read before its slot is rewritten)
 // Raw-moment order of fin: m000 m100 m010 m001 m200 m110 m101 m020 m011 m002; partial index
 // order (ay,az) = 00, 01, 02, 10, 11, 20 (b: 00, 01, 10).
+template <int LAT = 27>
 __device__ __forceinline__ void yx_stage(V (*exch)[kNW][32], int wu, int wd, int lane, const V zc[3][3],
-                                         const Part6& Mq, Part6& NqNn, const Part6& Np, V fin[10], Part6& nb) {
+                                         const Part6& Mq, Part6& NqNn, const Part6& Np, V fin[10], Part6& nb,
+                                         const V* zcb = nullptr) {
   const V c4 = vsplat(4.0f);
 #pragma unroll
   for (int az = 0; az < 3; ++az) {
-    V Y[3][3];   // [kx][ay]
+    V Y[3][3];   // [kx][ay]: chain A (D3Q27), or W = Y_A - Y_B (D3Q19)
+    V cen[3];    // D3Q19 centre terms 4 Y_A[0][ay] + 2 Y_B[0][ay]
+    bool zero1 = false;   // D3Q19, az = 1: W[kx][1] = 0 (chain B's ay = 1 output equals chain A's)
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx) {
-      const V A = exch[xslot(kx, 0, az)][wu][lane];
-      const V B = exch[xslot(kx, 1, az)][wd][lane];
-      const V S = vadd(A, B);
-      Y[kx][0] = vfma(zc[kx][az], c4, S);
-      if (az <= 1) Y[kx][1] = vsub(A, B);
-      if (az == 0) Y[kx][2] = S;
+      if constexpr (LAT == 19) {
+        if (az == 0) {
+          const V A = exch[xslot(kx, 0, 0)][wu][lane], B = exch[xslot(kx, 1, 0)][wd][lane];
+          const V AB = exch[xslotB(kx, 0)][wu][lane], BB = exch[xslotB(kx, 1)][wd][lane];
+          const V SA = vadd(A, B), SB = vadd(AB, BB);
+          const V YA0 = vfma(zc[kx][0], c4, SA), YB0 = vfma(zcb[kx], vsplat(2.0f), vneg(SB));
+          Y[kx][0] = vsub(YA0, YB0);
+          Y[kx][1] = vsub(vadd(A, AB), vadd(B, BB));
+          Y[kx][2] = vadd(SA, SB);
+          if (kx == 0) {
+            cen[0] = vfma(YA0, c4, vadd(YB0, YB0));
+            const V d = vsub(A, B), dB = vsub(BB, AB);
+            cen[1] = vfma(d, c4, vadd(dB, dB));
+            cen[2] = vfma(SA, c4, vmul(SB, -2.0f));
+          }
+        } else {
+          Y[kx][0] = vmul(zc[kx][az], 6.0f);
+          zero1 = (az == 1);
+          if (kx == 0) {   // only the centre column needs the exchanged values
+            const V A = exch[xslot(0, 0, az)][wu][lane], B = exch[xslot(0, 1, az)][wd][lane];
+            cen[0] = vmul(vfma(zc[0][az], vsplat(2.0f), vadd(A, B)), 6.0f);
+            if (az == 1) cen[1] = vmul(vsub(A, B), 6.0f);
+          }
+        }
+      } else {
+        const V A = exch[xslot(kx, 0, az)][wu][lane];
+        const V B = exch[xslot(kx, 1, az)][wd][lane];
+        const V S = vadd(A, B);
+        Y[kx][0] = vfma(zc[kx][az], c4, S);
+        if (az <= 1) Y[kx][1] = vsub(A, B);
+        if (az == 0) Y[kx][2] = S;
+      }
     }
 #pragma unroll
     for (int ay = 0; ay + az <= 2; ++ay) {
       const int c = ay == 0 ? az : (ay == 1 ? 3 + az : 5);          // partial index of (ay, az)
       const int m0 = ay == 0 ? (az == 0 ? 0 : (az == 1 ? 3 : 9)) : (ay == 1 ? (az == 0 ? 2 : 8) : 7);
+      if (LAT == 19 && zero1 && ay == 1) {   // W = 0: no neighbour contribution along x
+        fin[m0] = Mq.a[c];
+        nb.a[c] = vadd(cen[1], Np.a[c]);
+        NqNn.a[c] = vsplat(0.f);
+        continue;
+      }
       const V P = vadd(Y[0][ay], Y[2][ay]);
       const V Xp = vadd(P, Y[1][ay]);
       const V Xm = vsub(P, Y[1][ay]);
@@ -249,7 +326,8 @@ __device__ __forceinline__ void yx_stage(V (*exch)[kNW][32], int wu, int wd, int
         fin[m1] = vsub(NqNn.a[c], Xm);
       }
       if (ay + az == 0) fin[4] = vadd(NqNn.a[0], Xm);
-      nb.a[c] = vfma(Y[0][ay], c4, Np.a[c]);
+      if constexpr (LAT == 19) nb.a[c] = vadd(cen[ay], Np.a[c]);
+      else nb.a[c] = vfma(Y[0][ay], c4, Np.a[c]);
       NqNn.a[c] = Xp;
     }
   }
@@ -468,11 +546,12 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
   }
 }
 
-template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE, int STAGES, int NB>
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE, int STAGES, int NB, int LAT = 27>
 __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_constant__ StepArgs A) {
   constexpr int NC = Q16 ? 5 : 10;
+  using Sm = Smem<NC, STAGES, NB, LatSlots<LAT>::n>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Smem<NC, STAGES, NB>& S = *reinterpret_cast<Smem<NC, STAGES, NB>*>(smem_raw);
+  Sm& S = *reinterpret_cast<Sm*>(smem_raw);
   const Geo& g = A.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
@@ -542,14 +621,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         load_state<Q16, QMODE, !FORCE>(S.stage[st], 0, lane, inflow, A, s);
         const Coef<V> C = coeffs_int<FORCE, Q16>(s, A.R);
         if (!do_hi) consumed();
-        recon_halo<0>(C, S.exch[b], 0, lane);
+        recon_halo<0, LAT>(C, S.exch[b], 0, lane);
       }
       if (do_hi) {
         V s[10];
         load_state<Q16, QMODE, !FORCE>(S.stage[st], kBoxRows - 1, lane, inflow, A, s);
         const Coef<V> C = coeffs_int<FORCE, Q16>(s, A.R);
         consumed();
-        recon_halo<1>(C, S.exch[b], xrow, lane);
+        recon_halo<1, LAT>(C, S.exch[b], xrow, lane);
       }
       mbar_arrive(&S.full[b][xrow]);
       // producer (warp 0): once every warp has read plane it, its stage takes plane it + STAGES
@@ -579,6 +658,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
       mbar_wait(&S.bar[st], sph);
       V fin[10];   // dest q, raw-moment order m000 m100 m010 m001 m200 m110 m101 m020 m011 m002
       V zcen[3][3];  // [kx][az]: ky = 0 z-stage values of this source row (y centre term)
+      V zcb[3];      // D3Q19: chain B's az = 0 centre values
       {
         V s[10];
         load_state<Q16, QMODE, !FORCE>(S.stage[st], w, lane, plane_inflow(p), A, s);
@@ -586,15 +666,15 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
         consumed();   // C depends on every loaded value
         // my slots of buffer b were read by my neighbours NB planes ago
         mbar_wait(&S.empty[b][w], eph ^ 1u);
-        recon_row<0>(C, exch, w, lane, zcen[0]);
-        recon_row<1>(C, exch, w, lane, zcen[1]);
-        recon_row<2>(C, exch, w, lane, zcen[2]);
+        recon_row<0, LAT>(C, exch, w, lane, zcen[0], &zcb[0]);
+        recon_row<1, LAT>(C, exch, w, lane, zcen[1], &zcb[1]);
+        recon_row<2, LAT>(C, exch, w, lane, zcen[2], &zcb[2]);
       }
       if (++st == STAGES) { st = 0; sph ^= 1u; }
       mbar_arrive(&S.full[b][w]);
       mbar_wait(&S.full[b][wu], eph);
       mbar_wait(&S.full[b][wd], eph);
-      yx_stage(exch, wu, wd, lane, zcen, Mq, NqNn, Np, fin, nb);
+      yx_stage<LAT>(exch, wu, wd, lane, zcen, Mq, NqNn, Np, fin, nb, zcb);
       mbar_arrive(&S.empty[b][wu]);
       mbar_arrive(&S.empty[b][wd]);
       if (store_plane) {
@@ -669,17 +749,18 @@ __global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_const
 #ifndef HLBM_F32_NB
 #define HLBM_F32_NB 1   // fp32 tiles leave room for one exchange buffer next to 3 stages
 #endif
-template <bool Q16> struct InteriorCfg {
-  static constexpr int STAGES = Q16 ? HLBM_Q16_STAGES : HLBM_F32_STAGES;
+template <bool Q16, int LAT = 27> struct InteriorCfg {
+  // fp32 D3Q19: the 24-slot exchange leaves room for 2 TMA stages only (227 KB per CTA)
+  static constexpr int STAGES = Q16 ? HLBM_Q16_STAGES : (LAT == 19 ? 2 : HLBM_F32_STAGES);
   static constexpr int NB = Q16 ? HLBM_Q16_NB : HLBM_F32_NB;
 };
 
-template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE>
+template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE, int LAT = 27>
 static cudaError_t launch_interior_t(const StepArgs& A, int nblocks, cudaStream_t st) {
-  constexpr int STAGES = InteriorCfg<Q16>::STAGES, NB = InteriorCfg<Q16>::NB;
+  constexpr int STAGES = InteriorCfg<Q16, LAT>::STAGES, NB = InteriorCfg<Q16, LAT>::NB;
   constexpr int NC = Q16 ? 5 : 10;
-  const size_t smem = sizeof(Smem<NC, STAGES, NB>);
-  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STATS, QMODE, STAGES, NB>;
+  const size_t smem = sizeof(Smem<NC, STAGES, NB, LatSlots<LAT>::n>);
+  auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STATS, QMODE, STAGES, NB, LAT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<nblocks, kNW * 32, smem, st>>>(A);
