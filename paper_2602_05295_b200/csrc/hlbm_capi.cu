@@ -221,16 +221,10 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   StepArgs A = make_args(ctx, with_stats, xb, xr);
-  if (ctx->q == 19 && !special && (!q16 || ctx->qmode == 2)) {
-    // D3Q19 fluid-only: the interior kernel with two-chain streaming (no boundary lists)
-    CK(launch_fluid_interior19(A, q16, force, dither, ctx->stream));
-    ++ctx->launches;
-    if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
-    return fix_one_row(ctx);
-  }
-  if (ctx->q == 19) {
-    // D3Q19 with solids or a non-default codec: the per-cell fused kernel over the planes of the
-    // range, solid links inline
+  const bool fast19 = ctx->q == 19 && (!q16 || ctx->qmode == 2);
+  if (ctx->q == 19 && !fast19) {
+    // D3Q19 with a non-default codec: the per-cell fused kernel over the planes of the range,
+    // solid links inline
     const int64_t pl = (int64_t)ctx->cfg.ny * ctx->cfg.nz;
     CK(launch_pull_cells(A, nullptr, ctx->d_fused, (int64_t)(xr - xb) * pl, 3, q16, force, dither, ctx->stream, 19,
                          (int64_t)xb * pl));
@@ -238,7 +232,10 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
     if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
     return fix_one_row(ctx);
   }
-  CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
+  if (fast19)   // D3Q19: two-chain streaming; solids through the compacted 19-link kernels below
+    CK(launch_fluid_interior19(A, q16, force, special, dither, ctx->stream));
+  else
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
   ++ctx->launches;
   if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
   auto sub = [&](const std::vector<int64_t>& off, int64_t n, int64_t& a, int64_t& cnt) {
@@ -249,12 +246,12 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   int64_t a, cnt;
   sub(ctx->off_b, ctx->nb, a, cnt);
   if (cnt > 0) {
-    CK(launch_pull_cells(A, ctx->d_bcells + a, ctx->d_bmasks + a, cnt, 0, q16, force, dither, ctx->stream));
+    CK(launch_pull_cells(A, ctx->d_bcells + a, ctx->d_bmasks + a, cnt, 0, q16, force, dither, ctx->stream, ctx->q));
     ++ctx->launches;
   }
   sub(ctx->off_s, ctx->ns, a, cnt);
   if (cnt > 0) {
-    CK(launch_pull_cells(A, ctx->d_scells + a, nullptr, cnt, 1, q16, force, dither, ctx->stream));
+    CK(launch_pull_cells(A, ctx->d_scells + a, nullptr, cnt, 1, q16, force, dither, ctx->stream, ctx->q));
     ++ctx->launches;
   }
   sub(ctx->off_m, ctx->mesh.nb, a, cnt);

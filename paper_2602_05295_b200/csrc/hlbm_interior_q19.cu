@@ -1,15 +1,19 @@
-// D3Q19 variants of fluid_interior (LAT = 19; hlbm_interior.cuh, two-chain streaming): fluid-only
-// slabs, fp32 or 16-bit codes with the default QuantSpec (codec mode 2).
+// D3Q19 variants of fluid_interior (LAT = 19; hlbm_interior.cuh, two-chain streaming): fp32 or
+// 16-bit codes with the default QuantSpec (codec mode 2); solids through the compacted kernels.
 #include "hlbm_interior.cuh"
 #include "hlbm_launch.h"
 
 namespace hlbm {
 
-cudaError_t launch_fluid_interior19(const StepArgs& A, bool q16, bool force, bool dither, cudaStream_t st) {
+cudaError_t launch_fluid_interior19(const StepArgs& A, bool q16, bool force, bool special, bool dither,
+                                    cudaStream_t st) {
   const int nblocks = A.g.nzt * A.g.nyt * A.g.nxs;
   if (nblocks == 0) return cudaSuccess;
   const bool stats = A.do_stats != 0;
-#define HLBM_Q19(Q, F, D, S, M) return launch_interior_t<Q, F, false, D, S, M, 19>(A, nblocks, st)
+  // SPECIAL only changes the statistics (boundary / solid cells are finished by pull_cells)
+#define HLBM_Q19(Q, F, D, S, M)                                                     \
+  return (S && special) ? launch_interior_t<Q, F, true, D, S, M, 19>(A, nblocks, st) \
+                        : launch_interior_t<Q, F, false, D, S, M, 19>(A, nblocks, st)
   if (!q16) {
     if (force) { if (stats) HLBM_Q19(false, true, false, true, 0); HLBM_Q19(false, true, false, false, 0); }
     if (stats) HLBM_Q19(false, false, false, true, 0);
