@@ -56,8 +56,9 @@ typedef struct hlbm_config {
   uint32_t seed;
   int32_t device;              /* CUDA device ordinal                                         */
   int32_t xseg;                /* interior-kernel x segment length (0 = default)              */
-  int32_t q;                   /* velocity set: 27 (D3Q27, default when 0) or 19 (D3Q19: per-cell
-                                  fused kernel only, voxel solids; lattice.py:172-211)           */
+  int32_t q;                   /* velocity set: 27 (D3Q27, default when 0) or 19 (D3Q19:
+                                  two-chain interior kernel + 19-link compacted kernels; voxel
+                                  solids only; lattice.py:172-211)                               */
 } hlbm_config;
 
 /* StepStats. Sums run over fluid cells of this slab. */

@@ -165,7 +165,7 @@ class Solver:
         c.seed = int(config.seed) & 0xFFFFFFFF
         c.device = int(config.device)
         c.xseg = int(config.xseg)
-        c.q = 19 if config.lattice.upper() == "D3Q19" else 27   # D3Q19: per-cell fused kernel
+        c.q = 19 if config.lattice.upper() == "D3Q19" else 27   # D3Q19: two-chain streaming
         ctx = C.c_void_p()
         rc = self._lib.hlbm_create(C.byref(c), C.byref(ctx))
         self._ctx = ctx
