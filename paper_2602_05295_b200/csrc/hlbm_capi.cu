@@ -108,7 +108,7 @@ Geo make_geo(const hlbm_ctx* ctx, int xb = 0, int xr = -1) {
   const int nr = std::max(xr - xb, 0);
   g.xb = xb;
   g.xr = xr;
-  g.xseg = c.xseg > 0 ? std::min(c.xseg, std::max(nr, 1)) : auto_xseg(std::max(nr, 1), g.nzt * g.nyt, ctx->num_sms);
+  g.xseg = c.xseg > 0 ? std::min(c.xseg, std::max(nr, 1)) : auto_xseg(std::max(nr, 1), g.nzt * g.nyt, ctx->num_sms * kCtaPerSm);
   g.nxs = nr > 0 ? (nr + g.xseg - 1) / g.xseg : 0;
   g.gx0 = c.x0; g.gny = c.gny; g.gnz = c.gnz; g.gnx_total = c.gnx;
   return g;

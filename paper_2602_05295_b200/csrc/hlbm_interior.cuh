@@ -547,7 +547,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
 }
 
 template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE, int STAGES, int NB, int LAT = 27>
-__global__ void __launch_bounds__(kNW * 32, 1) fluid_interior(const __grid_constant__ StepArgs A) {
+__global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __grid_constant__ StepArgs A) {
   constexpr int NC = Q16 ? 5 : 10;
   using Sm = Smem<NC, STAGES, NB, LatSlots<LAT>::n>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
