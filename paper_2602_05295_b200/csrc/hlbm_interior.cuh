@@ -439,6 +439,26 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
   const Geo& g = A.g;
   V s[10], inv;
   raw_to_state<V, Q16>(m, s, &inv);
+  if (STATS) {
+    // mass, momentum, max |u|^2 -- accumulated before the encode (shorter live ranges of s and
+    // 1/rho; measured 2.08 -> 2.02 ms for the STATS variant at 512^3) (NaN in any cell already makes the mass sum non-finite)
+    const V ju = vmul(vfma(s[3], s[3], vfma(s[2], s[2], vmul(s[1], s[1]))), vmul(inv, inv));
+    if (statx && staty) {
+      const V a = vadd(make_float2(s[0].x, s[1].x), make_float2(s[0].y, s[1].y));
+      const V c = vadd(make_float2(s[2].x, s[3].x), make_float2(s[2].y, s[3].y));
+      acc[0] += a.x; acc[32] += a.y; acc[64] += c.x; acc[96] += c.y;
+      acc[128] = fmaxf(acc[128], fmaxf(ju.x, ju.y));
+    } else {
+      if (statx) {
+        acc[0] += s[0].x; acc[32] += s[1].x; acc[64] += s[2].x; acc[96] += s[3].x;
+        acc[128] = fmaxf(acc[128], ju.x);
+      }
+      if (staty) {
+        acc[0] += s[0].y; acc[32] += s[1].y; acc[64] += s[2].y; acc[96] += s[3].y;
+        acc[128] = fmaxf(acc[128], ju.y);
+      }
+    }
+  }
   const int64_t plane_off = (int64_t)(q + 1) * g.pstride;
   const int64_t cell_off = plane_off + cell_off0;
   constexpr bool B16 = QMODE >= 1;
@@ -524,25 +544,6 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     }
     put_pair(g, reinterpret_cast<uint32_t*>(A.out) + cell_off, reinterpret_cast<uint32_t*>(A.out) + plane_off, y,
              z, wd, 5);
-  }
-  if (STATS) {
-    // mass, momentum, max |u|^2 (NaN in any cell already makes the mass sum non-finite)
-    const V ju = vmul(vfma(s[3], s[3], vfma(s[2], s[2], vmul(s[1], s[1]))), vmul(inv, inv));
-    if (statx && staty) {
-      const V a = vadd(make_float2(s[0].x, s[1].x), make_float2(s[0].y, s[1].y));
-      const V c = vadd(make_float2(s[2].x, s[3].x), make_float2(s[2].y, s[3].y));
-      acc[0] += a.x; acc[32] += a.y; acc[64] += c.x; acc[96] += c.y;
-      acc[128] = fmaxf(acc[128], fmaxf(ju.x, ju.y));
-    } else {
-      if (statx) {
-        acc[0] += s[0].x; acc[32] += s[1].x; acc[64] += s[2].x; acc[96] += s[3].x;
-        acc[128] = fmaxf(acc[128], ju.x);
-      }
-      if (staty) {
-        acc[0] += s[0].y; acc[32] += s[1].y; acc[64] += s[2].y; acc[96] += s[3].y;
-        acc[128] = fmaxf(acc[128], ju.y);
-      }
-    }
   }
 }
 
