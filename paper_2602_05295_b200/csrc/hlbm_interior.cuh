@@ -23,6 +23,9 @@
 //   * each input plane tile (64 z x 17 y x NC components) is ONE 4-D tensor TMA copy
 //     (cp.async.bulk.tensor + mbarrier) into shared memory, STAGES planes ahead; the y/z ghost
 //     layers of the layout make every tile in-bounds (no wrap).
+//   * LAT = 19 (D3Q19): a second streaming chain with the 1-D weights (2, -1, -1), merged with
+//     the D3Q27 chain in the x stage (see xslotB).
+//   * collision + Hermite run on inputs pre-scaled by the decode (coeffs_pre, hlbm_math.cuh).
 #pragma once
 #include "hlbm_params.cuh"
 
