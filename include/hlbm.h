@@ -151,6 +151,11 @@ int hlbm_next_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** 
  * Ranges of one step must be disjoint; their union must be [0, nx). */
 int hlbm_step_begin(hlbm_ctx* ctx, int32_t with_stats);
 int hlbm_step_range(hlbm_ctx* ctx, int32_t x_begin, int32_t x_end);
+/* step_range on an explicit CUDA stream (NULL: the context's): the edge planes of a slab run on a
+ * side stream concurrently with the bulk, whose launch would otherwise wait behind them.  The
+ * caller orders the streams (the side stream waits for the step's start; the context's stream
+ * waits for the side stream before step_end's successor). */
+int hlbm_step_range_on(hlbm_ctx* ctx, int32_t x_begin, int32_t x_end, void* cuda_stream);
 int hlbm_step_end(hlbm_ctx* ctx);
 /* device pointer of the current state buffer and its size (bytes) */
 int hlbm_state_buffer(hlbm_ctx* ctx, void** ptr, int64_t* bytes);

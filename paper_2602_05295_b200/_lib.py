@@ -81,6 +81,7 @@ SIGNATURES = {
                                         C.POINTER(C.c_int64)]),
     "hlbm_step_begin": (C.c_int, [_P, C.c_int32]),
     "hlbm_step_range": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "hlbm_step_range_on": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_void_p]),
     "hlbm_step_end": (C.c_int, [_P]),
     "hlbm_state_buffer": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64)]),
     "hlbm_step_count": (C.c_int64, [_P]),

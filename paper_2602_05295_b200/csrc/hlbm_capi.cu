@@ -208,16 +208,19 @@ int plane_offsets(hlbm_ctx* ctx, const int64_t* d_cells, int64_t n, std::vector<
 
 // a one-row slab (ny == 1): the interior kernel writes only the y = ny ghost image of an edge row;
 // refresh both ghost rows of the written buffer (tiny grids only, off the hot kernel)
-int fix_one_row(hlbm_ctx* ctx) {
+int fix_one_row(hlbm_ctx* ctx, cudaStream_t st) {
   if (ctx->cfg.ny != 1) return HLBM_OK;
-  CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], ctx->stream));
+  CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], st));
   ++ctx->launches;
   return HLBM_OK;
 }
 
-// interior kernel + compacted boundary kernels for destination planes [xb, xr)
-int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_interior = nullptr) {
+// interior kernel + compacted boundary kernels for destination planes [xb, xr), on stream st
+// (default: the context's stream)
+int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_interior = nullptr,
+              cudaStream_t st = nullptr) {
   if (xr <= xb) return HLBM_OK;
+  if (!st) st = ctx->stream;
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   StepArgs A = make_args(ctx, with_stats, xb, xr);
@@ -226,18 +229,18 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
     // D3Q19 with a non-default codec: the per-cell fused kernel over the planes of the range,
     // solid links inline
     const int64_t pl = (int64_t)ctx->cfg.ny * ctx->cfg.nz;
-    CK(launch_pull_cells(A, nullptr, ctx->d_fused, (int64_t)(xr - xb) * pl, 3, q16, force, dither, ctx->stream, 19,
+    CK(launch_pull_cells(A, nullptr, ctx->d_fused, (int64_t)(xr - xb) * pl, 3, q16, force, dither, st, 19,
                          (int64_t)xb * pl));
     ++ctx->launches;
-    if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
-    return fix_one_row(ctx);
+    if (after_interior) CK(cudaEventRecord(after_interior, st));
+    return fix_one_row(ctx, st);
   }
   if (fast19)   // D3Q19: two-chain streaming; solids through the compacted 19-link kernels below
-    CK(launch_fluid_interior19(A, q16, force, special, dither, ctx->stream));
+    CK(launch_fluid_interior19(A, q16, force, special, dither, st));
   else
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, ctx->stream));
+    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, st));
   ++ctx->launches;
-  if (after_interior) CK(cudaEventRecord(after_interior, ctx->stream));
+  if (after_interior) CK(cudaEventRecord(after_interior, st));
   auto sub = [&](const std::vector<int64_t>& off, int64_t n, int64_t& a, int64_t& cnt) {
     if (off.empty()) { a = 0; cnt = (xb == 0 && xr == ctx->cfg.nx) ? n : 0; return; }
     a = off[(size_t)xb];
@@ -246,22 +249,22 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   int64_t a, cnt;
   sub(ctx->off_b, ctx->nb, a, cnt);
   if (cnt > 0) {
-    CK(launch_pull_cells(A, ctx->d_bcells + a, ctx->d_bmasks + a, cnt, 0, q16, force, dither, ctx->stream, ctx->q));
+    CK(launch_pull_cells(A, ctx->d_bcells + a, ctx->d_bmasks + a, cnt, 0, q16, force, dither, st, ctx->q));
     ++ctx->launches;
   }
   sub(ctx->off_s, ctx->ns, a, cnt);
   if (cnt > 0) {
-    CK(launch_pull_cells(A, ctx->d_scells + a, nullptr, cnt, 1, q16, force, dither, ctx->stream, ctx->q));
+    CK(launch_pull_cells(A, ctx->d_scells + a, nullptr, cnt, 1, q16, force, dither, st, ctx->q));
     ++ctx->launches;
   }
   sub(ctx->off_m, ctx->mesh.nb, a, cnt);
   if (cnt > 0) {
     StepArgs Am = A;
     Am.cut_t = ctx->mesh.t32 + a * 27;
-    CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, ctx->stream));
+    CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, st));
     ++ctx->launches;
   }
-  return fix_one_row(ctx);
+  return fix_one_row(ctx, st);
 }
 
 }  // namespace
@@ -799,9 +802,13 @@ int hlbm_step_begin(hlbm_ctx* ctx, int32_t with_stats) {
 }
 
 int hlbm_step_range(hlbm_ctx* ctx, int32_t x_begin, int32_t x_end) {
+  return hlbm_step_range_on(ctx, x_begin, x_end, nullptr);
+}
+
+int hlbm_step_range_on(hlbm_ctx* ctx, int32_t x_begin, int32_t x_end, void* stream) {
   if (!ctx) return HLBM_EINVAL;
   if (x_begin < 0 || x_end > ctx->cfg.nx || x_begin > x_end) return fail(ctx, HLBM_EINVAL, "bad x range");
-  return run_range(ctx, x_begin, x_end, ctx->pending_stats);
+  return run_range(ctx, x_begin, x_end, ctx->pending_stats, nullptr, (cudaStream_t)stream);
 }
 
 int hlbm_step_end(hlbm_ctx* ctx) {

@@ -11,12 +11,12 @@ box, gloo in the CPU tests).  Ranks at a non-periodic x face have no neighbour t
 ghost plane is resolved by the BC inside the kernels (inflow constants / outflow clamp /
 wall bounce-back).
 
-Overlap: a step computes its two edge destination planes first
-(``step_range(0, 1)``, ``step_range(nx-1, nx)``), then posts the exchange of those planes
-into the neighbours' ghost planes of the buffer being written -- on a separate CUDA stream
-that waits only for the edge kernels -- while the bulk ``step_range(1, nx-1)`` runs on the
-compute stream.  The next step's kernels wait for the exchange with a stream event, never
-on the host.
+Overlap: a step computes its two edge destination planes
+(``step_range(0, 1)``, ``step_range(nx-1, nx)``) on a side stream while the bulk
+``step_range(1, nx-1)`` runs on the compute stream; the exchange of the edge planes into the
+neighbours' ghost planes of the buffer being written runs on a third stream that waits only
+for the edge kernels.  The next step's kernels wait for the edges and the exchange with stream
+events, never on the host.
 """
 
 from __future__ import annotations
@@ -137,11 +137,13 @@ class DistributedSolver:
                 solver.set_mask(np.asarray(mask)[p.x0:p.x0 + p.nx], gl, gh)
         self.solver = solver
         self._comm_stream = None
+        self._edge_stream = None
         self._comm_done = None
         if self._cuda:
             # kernels run on torch's current stream; the halo exchange on its own stream
             self.solver.set_stream(torch.cuda.current_stream().cuda_stream)
             self._comm_stream = torch.cuda.Stream()
+            self._edge_stream = torch.cuda.Stream()   # edge planes, concurrent with the bulk
         self._synced_version = None   # solver state version whose ghost planes are exchanged
 
     # ------------------------------------------------------------------ exchange
@@ -157,15 +159,16 @@ class DistributedSolver:
         t = self._halo_tensors(next_buffer)
         exchange_halos(t[0], t[1], t[2], t[3], self.plan, self.group)
 
-    def _post_exchange_next(self):
-        """Exchange the edge planes just written to the next buffer, overlapped with the bulk."""
+    def _post_exchange_next(self, edges_done=None):
+        """Exchange the edge planes just written to the next buffer, overlapped with the bulk
+        (`edges_done`: the event after the edge kernels; default: now on the compute stream)."""
         torch = self._torch
         if not self._cuda:
             self.exchange(next_buffer=True)
             return
-        compute = torch.cuda.current_stream()
-        edges_done = torch.cuda.Event()
-        edges_done.record(compute)
+        if edges_done is None:
+            edges_done = torch.cuda.Event()
+            edges_done.record(torch.cuda.current_stream())
         with torch.cuda.stream(self._comm_stream):
             self._comm_stream.wait_event(edges_done)
             self.exchange(next_buffer=True)          # NCCL work ordered on the comm stream
@@ -195,10 +198,28 @@ class DistributedSolver:
             s.step_end()
             self._synced_version = None                 # exchange at the next step's start
             return
-        s.step_range(0, 1)
-        s.step_range(nx - 1, nx)
-        self._post_exchange_next()
-        s.step_range(1, nx - 1)
+        if self._cuda:
+            # edge planes on a side stream, concurrently with the bulk on the compute stream (the
+            # bulk's launch does not queue behind the small, latency-bound edge launches); the
+            # exchange waits for the edges only; the next step waits for both streams
+            torch = self._torch
+            compute = torch.cuda.current_stream()
+            start = torch.cuda.Event()
+            start.record(compute)
+            self._edge_stream.wait_event(start)
+            es = self._edge_stream.cuda_stream
+            s.step_range(0, 1, es)
+            s.step_range(nx - 1, nx, es)
+            edges_done = torch.cuda.Event()
+            edges_done.record(self._edge_stream)
+            self._post_exchange_next(edges_done)
+            s.step_range(1, nx - 1)
+            compute.wait_event(edges_done)
+        else:
+            s.step_range(0, 1)
+            s.step_range(nx - 1, nx)
+            self._post_exchange_next()
+            s.step_range(1, nx - 1)
         s.step_end()
         self._synced_version = self._state_version()
 

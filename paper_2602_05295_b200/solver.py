@@ -428,8 +428,13 @@ class Solver:
     def step_begin(self, with_stats: bool = False):
         self._chk(self._lib.hlbm_step_begin(self._ctx, int(with_stats)))
 
-    def step_range(self, x_begin: int, x_end: int):
-        self._chk(self._lib.hlbm_step_range(self._ctx, int(x_begin), int(x_end)))
+    def step_range(self, x_begin: int, x_end: int, stream_ptr: Optional[int] = None):
+        """Destination planes [x_begin, x_end) of the step in progress, on the solver's stream or
+        on `stream_ptr` (a CUDA stream handle; the caller orders it against the solver's stream)."""
+        if stream_ptr is None:
+            self._chk(self._lib.hlbm_step_range(self._ctx, int(x_begin), int(x_end)))
+        else:
+            self._chk(self._lib.hlbm_step_range_on(self._ctx, int(x_begin), int(x_end), C.c_void_p(int(stream_ptr))))
 
     def step_end(self):
         self.state_version += 1
