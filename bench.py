@@ -9,6 +9,9 @@ GPU, NCCL halo exchange).  Synthetic initial state: solenoidal random Fourier mo
 1 <= |k| <= 4, u_rms = 0.05, seed 0; nu = 1e-4.  The headline `value` is the 16-bit path;
 the fp32 path is measured in the same run and reported beside it.
 
+``--strong`` runs SURVEY.md §8d config 5 instead: a 2048 x 512 x 512 global grid split into N
+x-slabs (strong scaling).
+
 Emits ONE JSON line on rank 0.  `--impl reference` times the reference's own CPU
 implementation of the step (momentlbm from baseline/_ref, else the oracle port) on the
 host cores instead.
@@ -33,6 +36,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "MLUPS (1/2/4/8 B200) and % of HBM roofline, fp32 vs 16-bit moments"
 BYTES_PER_CELL = {"q16": 40, "fp32": 80}     # algorithmic HBM bytes per cell update
 N_PER_GPU = 512
+STRONG_NX = 2048      # SURVEY.md §8d config 5 global x extent (bench.py --strong)
 
 
 def peaks():
@@ -183,14 +187,17 @@ def _dist_env():
     return world, rank, local
 
 
-def _make(precision, world, rank, local):
+def _make(precision, world, rank, local, gnx=None):
+    """Weak scaling (default): (512 N) x 512 x 512, the same field on every slab.  Strong scaling
+    (gnx given): gnx x 512 x 512 split into N x-slabs."""
     from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
     from paper_2602_05295_b200.geometry import turbulence_modes
     cfg = SolverConfig(nu=1e-4, precision=precision, quant=QuantSpec(), device=local)
-    gdims = (N_PER_GPU * world, N_PER_GPU, N_PER_GPU)
+    gnx = N_PER_GPU * world if gnx is None else gnx
+    gdims = (gnx, N_PER_GPU, N_PER_GPU)
     modes = turbulence_modes(N_PER_GPU, seed=0)
     modes = modes.copy()
-    modes[:, 0] *= world     # same field per slab: wave numbers along x scale with the global nx
+    modes[:, 0] *= gnx // N_PER_GPU   # wave numbers along x scale with the global nx
     if world > 1:
         from paper_2602_05295_b200.distributed import DistributedSolver
         ds = DistributedSolver(gdims, cfg)
@@ -294,13 +301,17 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = peaks()
+    strong = args.strong
+    gnx = STRONG_NX if strong else N_PER_GPU * world
+    if gnx % world:
+        raise SystemExit(f"strong scaling needs {STRONG_NX} planes divisible by the GPU count")
     results = {}
     for precision in ("q16", "fp32"):
-        ds, s = _make(precision, world, rank, local)
+        ds, s = _make(precision, world, rank, local, gnx if strong else None)
         with ClockSampler(local) as clk:
             ms, launches = _timed(ds, s, args.steps, args.warmup, world)
         kt = _kernel_time(s)
-        cells = N_PER_GPU ** 3
+        cells = (gnx // world) * N_PER_GPU * N_PER_GPU      # this rank's slab
         achieved = cells * BYTES_PER_CELL[precision] / (kt * 1e-3) / 1e9
         tr = ncu_traffic(precision)
         results[precision] = {
@@ -326,11 +337,13 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(head["value"], 1), "unit": "MLUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: solenoidal random Fourier modes 1<=|k|<=4, u_rms=0.05, seed 0",
-        "config": {"workload": "BASELINE configs[1]: periodic fluid-only turbulence box, 16-bit moments "
-                               "(fp32 measured beside)",
-                   "grid_per_gpu": [N_PER_GPU] * 3, "global_grid": [N_PER_GPU * world, N_PER_GPU, N_PER_GPU],
+        "config": {"workload": ("SURVEY config 5 (strong scaling): periodic fluid-only turbulence box "
+                                f"{STRONG_NX}x512x512 in x-slabs, 16-bit moments (fp32 measured beside)") if strong else
+                               ("BASELINE configs[1]: periodic fluid-only turbulence box, 16-bit moments "
+                                "(fp32 measured beside)"),
+                   "grid_per_gpu": [gnx // world, N_PER_GPU, N_PER_GPU], "global_grid": [gnx, N_PER_GPU, N_PER_GPU],
                    "nu": 1e-4, "precision": "q16", "parallelism": f"x-slab dp{world}",
                    "l2": "inputs larger than L2: 2.7 GB (q16) / 5.4 GB (fp32) state per GPU vs 126 MB L2"},
         "roofline": head["roofline"],
@@ -382,6 +395,8 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: 2048x512x512 global grid split over the GPUs (default: weak, 512^3 per GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
