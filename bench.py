@@ -111,7 +111,8 @@ class ClockSampler:
 # ------------------------------------------------------------------------ reference arm (CPU)
 
 def _ref_modules():
-    """The reference's own functions (baseline/_ref install) or, if absent, the oracle port."""
+    """The reference's own functions (baseline/_ref install) or, if absent, the oracle port:
+    (kind, step over a periodic grid, step of a ghost-padded block -> its interior)."""
     ref = ROOT / "baseline" / "_ref"
     if (ref / "momentlbm").exists():
         sys.path.insert(0, str(ref))
@@ -119,63 +120,133 @@ def _ref_modules():
         import momentlbm.lattice as RL
         import momentlbm.moments as RM
         lat = RL.make_lattice("D3Q27")
+        vel = [tuple(int(c) for c in v) for v in lat.velocities]
 
         def step(rho, mom, stress, tau):
             r, m, s = RC.collide_moments(rho, mom, stress, None, tau, 3)
             f = RM.reconstruct_distributions(r, m, s, lat)
-            fs = np.stack([np.roll(f[i], shift=tuple(lat.velocities[i]), axis=(0, 1, 2)) for i in range(27)])
+            fs = np.stack([np.roll(f[i], shift=vel[i], axis=(0, 1, 2)) for i in range(27)])
             return RM.moments_from_distributions(fs, lat)
-        return "reference", step
+
+        def step_padded(rho, mom, stress, tau):
+            r, m, s = RC.collide_moments(rho, mom, stress, None, tau, 3)
+            f = RM.reconstruct_distributions(r, m, s, lat)
+            nx, ny, nz = (d - 2 for d in rho.shape)
+            fs = np.stack([f[i, 1 - cx:1 - cx + nx, 1 - cy:1 - cy + ny, 1 - cz:1 - cz + nz]
+                           for i, (cx, cy, cz) in enumerate(vel)])
+            return RM.moments_from_distributions(fs, lat)
+        return "reference", step, step_padded
     from oracle import step as OS  # the CPU oracle port (only the bench's reference leg uses it)
 
-    return "port", lambda rho, mom, stress, tau: OS.fluid_step(rho, mom, stress, tau)
+    return ("port", lambda rho, mom, stress, tau: OS.fluid_step(rho, mom, stress, tau),
+            lambda rho, mom, stress, tau: OS.step_padded(np.concatenate([rho[None], mom, stress]), tau))
 
 
-def _cpu_worker(args):
-    n, warmup, steps, seed = args
-    kind, step = _ref_modules()
+def _initial_state(n, x0=0, nx=None):
     from paper_2602_05295_b200.geometry import evaluate_modes, turbulence_modes
-    u = evaluate_modes(turbulence_modes(N_PER_GPU, seed=0), (n, n, n), origin=(seed * n, 0, 0),
-                       global_dims=(N_PER_GPU,) * 3)
-    rho = np.ones((n, n, n))
+    nx = n if nx is None else nx
+    u = evaluate_modes(turbulence_modes(N_PER_GPU, seed=0), (nx, n, n), origin=(x0, 0, 0), global_dims=(n, n, n))
+    rho = np.ones((nx, n, n))
     mom = rho * u
     stress = np.stack([mom[a] * u[b] for a, b in ((0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2))])
-    tau = 0.5 + 3e-4
+    return np.concatenate([rho[None], mom, stress])
+
+
+TAU = 0.5 + 3e-4
+
+
+def _single_core(n, warmup, steps):
+    """One process, one BLAS thread: the reference step of an n^3 periodic box."""
+    kind, step, _ = _ref_modules()
+    st = _initial_state(n)
+    rho, mom, stress = st[0], st[1:4], st[4:10]
     for _ in range(warmup):
-        rho, mom, stress = step(rho, mom, stress, tau)
+        rho, mom, stress = step(rho, mom, stress, TAU)
     t0 = time.perf_counter()
     for _ in range(steps):
-        rho, mom, stress = step(rho, mom, stress, tau)
-    return time.perf_counter() - t0, n ** 3 * steps, kind
+        rho, mom, stress = step(rho, mom, stress, TAU)
+    return time.perf_counter() - t0, kind
 
 
-def _cpu_procs(n):
-    """All host cores, bounded by memory (~2 KB per cell in flight for the NumPy reference)."""
+# x-slab workers: the state lives in two file-backed float64 arrays (10, n, n, n) shared by all
+# processes; each step every worker reads its planes x0-1 .. x1 (periodic halos, one plane per side)
+# from the current array and writes its planes x0 .. x1-1 of the other one
+_SLAB = {}
+
+
+def _slab_init(paths, n):
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    _SLAB["bufs"] = [np.memmap(p, dtype=np.float64, mode="r+", shape=(10, n, n, n)) for p in paths]
+    _SLAB["n"] = n
+    _SLAB["step"] = _ref_modules()[2]
+
+
+def _slab_step(args):
+    x0, x1, src = args
+    n = _SLAB["n"]
+    a, b = _SLAB["bufs"][src], _SLAB["bufs"][1 - src]
+    xs = [(x0 - 1) % n] + list(range(x0, x1)) + [x1 % n]
+    blk = np.asarray(a[:, xs])
+    blk = np.concatenate([blk[:, :, -1:], blk, blk[:, :, :1]], axis=2)       # periodic y ghosts
+    blk = np.concatenate([blk[:, :, :, -1:], blk, blk[:, :, :, :1]], axis=3)  # periodic z ghosts
+    r, m, s = _SLAB["step"](blk[0], blk[1:4], blk[4:10], TAU)
+    b[0, x0:x1] = r
+    b[1:4, x0:x1] = m
+    b[4:10, x0:x1] = s
+    return x1 - x0
+
+
+def cpu_reference(steps, warmup=1, n=128, procs=None, single_n=64, single_steps=2):
+    """Reference CPU path on the host cores: an n^3 periodic box split into
+    `procs` x-slabs with one-plane halos, one process per core (steps timed after `warmup`), plus
+    the single-core figure of a single_n^3 box (one process, OPENBLAS_NUM_THREADS=1)."""
+    import multiprocessing as mp
+    import tempfile
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"          # inherited by the spawned workers before numpy loads
+    procs = procs or _cpu_procs(max(1, n // (os.cpu_count() or 1)) * n * n)
+    procs = max(1, min(procs, n))
+    ctx = mp.get_context("spawn")
+    with tempfile.TemporaryDirectory(dir="/tmp") as tmp:
+        paths = [os.path.join(tmp, f"state{b}.f64") for b in range(2)]
+        for p in paths:
+            np.memmap(p, dtype=np.float64, mode="w+", shape=(10, n, n, n)).flush()
+        init = np.memmap(paths[0], dtype=np.float64, mode="r+", shape=(10, n, n, n))
+        init[:] = _initial_state(n)
+        init.flush()
+        del init
+        bounds = np.linspace(0, n, procs + 1).astype(int)
+        with ctx.Pool(procs, initializer=_slab_init, initargs=(paths, n)) as pool:
+            src = 0
+            for _ in range(warmup):
+                pool.map(_slab_step, [(bounds[i], bounds[i + 1], src) for i in range(procs)])
+                src = 1 - src
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                pool.map(_slab_step, [(bounds[i], bounds[i + 1], src) for i in range(procs)])
+                src = 1 - src
+            dt = time.perf_counter() - t0
+    with ctx.Pool(1) as pool:
+        t1, kind = pool.apply(_single_core, (single_n, 1, single_steps))
+    return {"mlups": n ** 3 * steps / dt / 1e6, "kind": kind, "cores": procs, "timed_s": dt,
+            "sample": f"{n}^3 periodic turbulence box in {procs} x-slabs with one-plane halos (one process per "
+                      f"core, OPENBLAS_NUM_THREADS=1, shared file-backed state), {steps} timed steps after {warmup} warm-up",
+            "single_core": {"value": round(single_n ** 3 * single_steps / t1 / 1e6, 3), "unit": "MLUPS", "cores": 1,
+                            "sample": f"{single_n}^3 periodic box, {single_steps} timed steps, one process, "
+                                      "OPENBLAS_NUM_THREADS=1"}}
+
+
+def _cpu_procs(cells_per_proc):
+    """All host cores, bounded by memory (~2.5 KB per cell in flight for the NumPy reference)."""
     procs = os.cpu_count() or 1
     try:
         import psutil
         avail = psutil.virtual_memory().available
-        procs = max(1, min(procs, int(0.5 * avail / (2500 * n ** 3))))
+        procs = max(1, min(procs, int(0.5 * avail / (2500 * cells_per_proc))))
     except Exception:
         pass
     return procs
-
-
-def cpu_reference(steps, warmup=1, n=48, procs=None):
-    """Reference CPU path on the host cores: `procs` processes, each stepping an independent n^3
-    periodic block of the same synthetic workload (warmup untimed steps, then `steps` timed)."""
-    import multiprocessing as mp
-    procs = procs or _cpu_procs(n)
-    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ[k] = "1"          # inherited by the spawned workers before numpy loads
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(procs) as pool:
-        res = pool.map(_cpu_worker, [(n, warmup, steps, i) for i in range(procs)])
-    cells = sum(r[1] for r in res)
-    per_proc = max(r[0] for r in res)
-    return {"mlups": cells / per_proc / 1e6, "kind": res[0][2], "cores": procs, "timed_s": per_proc,
-            "sample": f"{procs} processes x {steps} timed steps (after {warmup} warm-up) of an independent "
-                      f"{n}^3 periodic block each, OPENBLAS_NUM_THREADS=1"}
 
 
 # ------------------------------------------------------------------------ GPU arm
@@ -243,17 +314,20 @@ def _timed(ds, s, steps, warmup, world):
     return ms, launches
 
 
-def _kernel_time(s, reps=10):
-    """Average fluid_interior launch duration on this rank (one launch per fluid-only step)."""
+def _sustained(ds, s, world, local, seconds=2.0):
+    """Steady-state throughput: about `seconds` of back-to-back steps after the burst-timed region
+    (the chip settles at its power cap in long runs), with the clocks sampled during it."""
     import torch
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.step_async(2, with_stats=False)
-    torch.cuda.synchronize()
-    e0.record()
-    s.step_async(reps, with_stats=False)
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    import torch.distributed as dist
+    probe, _ = _timed(ds, s, 20, 0, world)
+    n = max(50, int(seconds * 1e3 / (probe / 20)))
+    if world > 1:   # every rank must run the same count
+        t = torch.tensor([n], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n = int(t.item())
+    with ClockSampler(local) as clk:
+        ms, _ = _timed(ds, s, n, 0, world)
+    return ms, n, clk.summary()
 
 
 def _e2e(ds, s, world, steps):
@@ -306,12 +380,16 @@ def run_ours(args):
     if gnx % world:
         raise SystemExit(f"strong scaling needs {STRONG_NX} planes divisible by the GPU count")
     results = {}
+    e2e = None
     for precision in ("q16", "fp32"):
         ds, s = _make(precision, world, rank, local, gnx if strong else None)
         with ClockSampler(local) as clk:
             ms, launches = _timed(ds, s, args.steps, args.warmup, world)
-        kt = _kernel_time(s)
         cells = (gnx // world) * N_PER_GPU * N_PER_GPU      # this rank's slab
+        # roofline of the timed region itself: at N = 1 a fluid-only step is exactly one
+        # fluid_interior launch (gpu_launches == steps), so the per-launch time is ms / steps;
+        # at N > 1 a step is the edge + bulk launches of the slab and the figure covers both
+        kt = ms / args.steps
         achieved = cells * BYTES_PER_CELL[precision] / (kt * 1e-3) / 1e9
         tr = ncu_traffic(precision)
         results[precision] = {
@@ -322,10 +400,15 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": tr, "peak_kind": peak_kind,
                          "kernel": "fluid_interior", "kernel_ms": round(kt, 4),
+                         "kernel_ms_from": "timed region (CUDA events on the launching stream) / steps",
                          "algorithmic_bytes_per_launch": cells * BYTES_PER_CELL[precision]},
         }
+        sms, sn, sclk = _sustained(ds, s, world, local)
+        results[precision]["sustained"] = {"value": round(cells * world * sn / (sms * 1e-3) / 1e6, 1),
+                                           "unit": "MLUPS", "steps": sn, "seconds": round(sms * 1e-3, 2),
+                                           "ms_per_step": round(sms / sn, 4), "clocks": sclk}
         if precision == "q16":
-            e2e = _e2e(ds, s, world, max(args.steps, 50))
+            e2e = _e2e(ds, s, world, max(args.steps, 200))
         if ds is not None:
             ds.solver.close()
         else:
@@ -345,20 +428,24 @@ def run_ours(args):
                                 "(fp32 measured beside)"),
                    "grid_per_gpu": [gnx // world, N_PER_GPU, N_PER_GPU], "global_grid": [gnx, N_PER_GPU, N_PER_GPU],
                    "nu": 1e-4, "precision": "q16", "parallelism": f"x-slab dp{world}",
-                   "l2": "inputs larger than L2: 2.7 GB (q16) / 5.4 GB (fp32) state per GPU vs 126 MB L2"},
+                   "l2": f"inputs larger than L2: {2 * 20 * (gnx // world) * N_PER_GPU ** 2 / 1e9:.1f} GB (q16) / "
+                         f"{2 * 40 * (gnx // world) * N_PER_GPU ** 2 / 1e9:.1f} GB (fp32) of double-buffered state "
+                         "per GPU vs 126 MB L2"},
         "roofline": head["roofline"],
         "clocks": head["clocks"],
+        "sustained": head["sustained"],
         "gpu_launches": head["launches"],
         "fp32": {"value": round(results["fp32"]["value"], 1), "unit": "MLUPS",
                  "ms_per_step": round(results["fp32"]["ms_per_step"], 4), "roofline": results["fp32"]["roofline"],
-                 "clocks": results["fp32"]["clocks"], "gpu_launches": results["fp32"]["launches"]},
+                 "clocks": results["fp32"]["clocks"], "gpu_launches": results["fp32"]["launches"],
+                 "sustained": results["fp32"]["sustained"]},
         "paper_ref": {"value": 7097, "unit": "MLUPS", "what": "paper fluid-only 1024^3 16-bit on a 6912-core 80 GB GPU (PAPER.md:855)"},
     }
     if e2e is not None:
         line["e2e"] = e2e
     if cpu is not None:
         line["cpu_baseline"] = {"value": round(cpu["mlups"], 3), "unit": "MLUPS", "cores": cpu["cores"],
-                                "kind": cpu["kind"], "sample": cpu["sample"]}
+                                "kind": cpu["kind"], "sample": cpu["sample"], "single_core": cpu["single_core"]}
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -368,25 +455,47 @@ def run_ours(args):
 
 
 def run_reference(args):
-    """The reference's own CPU implementation on all host cores (rank 0 only)."""
+    """The reference's own CPU implementation on all host cores (rank 0 only): the 128^3 sample of
+    the turbulence-box workload in x-slabs with one-plane halos, one process per core."""
     world, rank, local = _dist_env()
     if rank != 0:
         return
-    n = 48
-    steps = max(1, min(args.steps, 20))      # bounded: the whole run stays within a few minutes
-    res = cpu_reference(steps=steps, warmup=min(max(args.warmup, 1), 3), n=n)
+    n = int(os.environ.get("BENCH_REF_N", "128"))   # (the CPU tests shrink the sample)
+    steps = max(1, min(args.steps, 10))      # bounded: the whole run stays within a few minutes
+    res = cpu_reference(steps=steps, warmup=min(max(args.warmup, 1), 2), n=n, single_n=min(64, n))
     v = res["mlups"]
-    line = {"metric": METRIC, "value": round(v, 3), "unit": "MLUPS", "n_gpus": world, "steps": steps,
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "MLUPS", "n_gpus": args.gpus, "steps": steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * res["timed_s"] / steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "impl": "reference",
             "data": "synthetic: solenoidal random Fourier modes 1<=|k|<=4, u_rms=0.05, seed 0",
-            "config": {"workload": "BASELINE configs[1] sample: periodic fluid-only turbulence box blocks "
-                                   f"({n}^3 per host core)", "precision": "float64 (reference NumPy)"},
+            "config": {"workload": "BASELINE configs[1] sample: periodic fluid-only turbulence box "
+                                   f"{n}^3 in x-slabs over the host cores", "precision": "float64 (reference NumPy)"},
             "cpu_baseline": {"value": round(v, 3), "unit": "MLUPS", "cores": res["cores"], "kind": res["kind"],
-                             "sample": res["sample"]},
+                             "sample": res["sample"], "single_core": res["single_core"]},
             "e2e": {"value": round(v, 3), "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def self_launch_cmd(argv, gpus, port=None):
+    """`bench.py --gpus N` started without a launcher re-executes itself under torchrun with N
+    ranks on this node (rendezvous on 127.0.0.1), so `--gpus N` always means N ranks."""
+    if port is None:
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + list(argv)
+
+
+def check_world(gpus, world, visible):
+    """Fail loudly unless the launched world is exactly --gpus ranks with a GPU each."""
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}: the launched world must equal --gpus")
+    if visible is not None and visible < gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but only {visible} CUDA device(s) are visible")
 
 
 def main():
@@ -400,6 +509,16 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(subprocess.call(self_launch_cmd(sys.argv[1:], args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        check_world(args.gpus, world, None)     # CPU arm: rank 0 runs, the others exit 0
+    else:
+        import torch
+        check_world(args.gpus, world, torch.cuda.device_count())
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -38,8 +38,12 @@ extern "C" {
 
 typedef struct hlbm_ctx hlbm_ctx;
 
-/* SolverConfig + SimGrid dims + QuantSpec. */
+/* SolverConfig + SimGrid dims + QuantSpec.
+ * ABI guard: the caller sets struct_size = sizeof(hlbm_config) (hlbm_config_init does); hlbm_create
+ * rejects any other value with HLBM_EINVAL before reading past the first field, so a binding built
+ * against a different layout fails loudly instead of reading garbage. */
 typedef struct hlbm_config {
+  int32_t struct_size;         /* sizeof(hlbm_config) of the caller's layout (352 bytes here)   */
   int32_t nx, ny, nz;          /* local interior dims of this slab (x is the slab axis)       */
   int32_t gnx, gny, gnz;       /* global dims (== local on one GPU)                           */
   int32_t x0;                  /* slab offset along x in the global grid                      */
@@ -51,7 +55,7 @@ typedef struct hlbm_config {
   double u_in[3];              /* inflow velocity                                             */
   int32_t precision;           /* HLBM_FP32 or HLBM_Q16                                       */
   double qmin[10], qmax[10];   /* codec ranges (rho, rho u_xyz, sneq xx..zz) */
-  int32_t bits[10];            /* bits per component, 8..16                 */
+  int32_t bits[10];            /* bits per component, 2..16                 */
   int32_t dither;              /* 1: counter-hash dither                         */
   uint32_t seed;
   int32_t device;              /* CUDA device ordinal                                         */
@@ -76,6 +80,9 @@ typedef struct hlbm_stats {
 } hlbm_stats;
 
 const char* hlbm_version(void);
+/* defaults: struct_size, periodic faces, fp32, the default QuantSpec ranges and
+ * 16 bits per component, D3Q27, device 0; the caller then sets dims and tau */
+void hlbm_config_init(hlbm_config* cfg);
 /* number of visible CUDA devices (0 when no driver / GPU) */
 int hlbm_device_count(void);
 

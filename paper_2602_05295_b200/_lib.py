@@ -21,6 +21,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libhlbm.so"
 
 class HlbmConfig(C.Structure):
     _fields_ = [
+        ("struct_size", C.c_int32),
         ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
         ("gnx", C.c_int32), ("gny", C.c_int32), ("gnz", C.c_int32),
         ("x0", C.c_int32), ("x_lo_remote", C.c_int32), ("x_hi_remote", C.c_int32),
@@ -49,6 +50,7 @@ _DP = C.POINTER(C.c_double)
 SIGNATURES = {
     "hlbm_version": (C.c_char_p, []),
     "hlbm_device_count": (C.c_int, []),
+    "hlbm_config_init": (None, [C.POINTER(HlbmConfig)]),
     "hlbm_create": (C.c_int, [C.POINTER(HlbmConfig), C.POINTER(_P)]),
     "hlbm_destroy": (None, [_P]),
     "hlbm_last_error": (C.c_char_p, [_P]),

@@ -207,10 +207,11 @@ int plane_offsets(hlbm_ctx* ctx, const int64_t* d_cells, int64_t n, std::vector<
 }
 
 // a one-row slab (ny == 1): the interior kernel writes only the y = ny ghost image of an edge row;
-// refresh both ghost rows of the written buffer (tiny grids only, off the hot kernel)
-int fix_one_row(hlbm_ctx* ctx, cudaStream_t st) {
+// refresh both ghost rows of the planes [xb, xr) of the written buffer (tiny grids only, off the
+// hot kernel; only the range's own planes, so ranges on concurrent streams stay independent)
+int fix_one_row(hlbm_ctx* ctx, int xb, int xr, cudaStream_t st) {
   if (ctx->cfg.ny != 1) return HLBM_OK;
-  CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], st));
+  CK(launch_fill_ghosts(make_geo(ctx, xb, xr), ctx->NC, ctx->buf[1 - ctx->cur], st));
   ++ctx->launches;
   return HLBM_OK;
 }
@@ -233,7 +234,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
                          (int64_t)xb * pl));
     ++ctx->launches;
     if (after_interior) CK(cudaEventRecord(after_interior, st));
-    return fix_one_row(ctx, st);
+    return fix_one_row(ctx, xb, xr, st);
   }
   if (fast19)   // D3Q19: two-chain streaming; solids through the compacted 19-link kernels below
     CK(launch_fluid_interior19(A, q16, force, special, dither, st));
@@ -264,7 +265,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
     CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, st));
     ++ctx->launches;
   }
-  return fix_one_row(ctx, st);
+  return fix_one_row(ctx, xb, xr, st);
 }
 
 }  // namespace
@@ -284,17 +285,35 @@ int hlbm_device_count(void) {
 
 const char* hlbm_last_error(const hlbm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+void hlbm_config_init(hlbm_config* cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->struct_size = (int32_t)sizeof(hlbm_config);
+  static const double dmn[10] = {0.8, -0.6, -0.6, -0.6, -0.1, -0.1, -0.1, -0.1, -0.1, -0.1};
+  static const double dmx[10] = {1.5, 0.6, 0.6, 0.6, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1};
+  for (int k = 0; k < 10; ++k) {
+    cfg->qmin[k] = dmn[k];
+    cfg->qmax[k] = dmx[k];
+    cfg->bits[k] = 16;
+  }
+  cfg->q = 27;
+}
+
 int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
   if (!cfg || !out) return HLBM_EINVAL;
   *out = nullptr;
   hlbm_ctx* ctx = new hlbm_ctx();
-  ctx->cfg = *cfg;
-  hlbm_config& c = ctx->cfg;
   auto bad = [&](const std::string& m) {
     int r = fail(ctx, HLBM_EINVAL, m);
     *out = ctx;   // caller reads the message, then destroys
     return r;
   };
+  // ABI guard: read only the size field until the caller's layout is known to match
+  if (cfg->struct_size != (int32_t)sizeof(hlbm_config))
+    return bad("hlbm_config.struct_size is " + std::to_string(cfg->struct_size) + ", this library expects " +
+               std::to_string(sizeof(hlbm_config)) + " (binding built against another hlbm.h)");
+  ctx->cfg = *cfg;
+  hlbm_config& c = ctx->cfg;
   if (c.nx < 1 || c.ny < 1 || c.nz < 4) return bad("grid dims must be >= 1 (nz >= 4)");
   if (c.nz % 4 != 0) return bad("nz must be a multiple of 4");
   if (c.gnx <= 0) c.gnx = c.nx;
@@ -404,6 +423,15 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
     CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[b], ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  // wall faces need the boundary lists even without a solid mask (the wall ghost layer is solid,
+  // its links bounce back): start from an all-fluid mask (a later hlbm_set_mask replaces it)
+  bool wall = false;
+  for (int f = 0; f < 6; ++f) wall = wall || c.bc[f] == HLBM_BC_WALL;
+  if (wall) {
+    const int64_t pl = (int64_t)c.ny * c.nz;
+    std::vector<uint8_t> zero((size_t)(pl * c.nx), 0);
+    if (int r = hlbm_set_mask(ctx, zero.data(), zero.data(), zero.data())) return r;
+  }
   return HLBM_OK;
 }
 

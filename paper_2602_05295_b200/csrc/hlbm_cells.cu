@@ -582,13 +582,14 @@ __global__ void init_modes(Geo g, Ranges R, void* dst, double rho0, const double
 }
 
 // copy edge columns of every interior row into the z ghost columns (periodic images)
+// planes [g.xb, g.xr) only: disjoint x-ranges of one step may run on concurrent streams
 __global__ void fill_ghosts(Geo g, int NC, uint32_t* buf) {
-  const int64_t n = (int64_t)g.nx * NC * 2 * g.ny;
+  const int64_t n = (int64_t)(g.xr - g.xb) * NC * 2 * g.ny;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pc = i / (2 * g.ny);
     const int k = (int)(i - pc * 2 * g.ny);
-    const int x = (int)(pc / NC), c = (int)(pc - (int64_t)x * NC);
+    const int xr = (int)(pc / NC), c = (int)(pc - (int64_t)xr * NC), x = g.xb + xr;
     uint32_t* row = buf + (int64_t)(x + 1) * g.pstride + (int64_t)c * g.cstride + (int64_t)((k >> 1) + 1) * g.zp;
     if (k & 1) row[g.nz + kZOff] = row[kZOff];            // z = nz  <- image of z = 0
     else row[kZOff - 1] = row[g.nz - 1 + kZOff];         // z = -1  <- image of z = nz-1
@@ -598,12 +599,12 @@ __global__ void fill_ghosts(Geo g, int NC, uint32_t* buf) {
 // ghost rows (after the columns are filled, so corners are consistent)
 __global__ void fill_ghost_rows(Geo g, int NC, uint32_t* buf) {
   const int rowsz = g.zp;   // whole padded rows (the z ghost columns included)
-  const int64_t n = (int64_t)g.nx * NC * 2 * rowsz;
+  const int64_t n = (int64_t)(g.xr - g.xb) * NC * 2 * rowsz;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pc = i / (2 * rowsz);
     const int k = (int)(i - pc * 2 * rowsz);
-    const int x = (int)(pc / NC), c = (int)(pc - (int64_t)x * NC);
+    const int xr = (int)(pc / NC), c = (int)(pc - (int64_t)xr * NC), x = g.xb + xr;
     uint32_t* base = buf + (int64_t)(x + 1) * g.pstride + (int64_t)c * g.cstride;
     const int zz = k >> 1;
     if (k & 1) base[(int64_t)(g.ny + 1) * g.zp + zz] = base[(int64_t)1 * g.zp + zz];
@@ -660,9 +661,10 @@ cudaError_t launch_export(const Geo& g, const Ranges& R, bool q16, const void* s
 }
 
 cudaError_t launch_fill_ghosts(const Geo& g, int NC, void* buf, cudaStream_t st) {
-  const int64_t n1 = (int64_t)g.nx * NC * 2 * g.ny;
+  if (g.xr <= g.xb) return cudaSuccess;
+  const int64_t n1 = (int64_t)(g.xr - g.xb) * NC * 2 * g.ny;
   fill_ghosts<<<grid_for(n1, 256), 256, 0, st>>>(g, NC, reinterpret_cast<uint32_t*>(buf));
-  const int64_t n2 = (int64_t)g.nx * NC * 2 * (g.nz + 2);
+  const int64_t n2 = (int64_t)(g.xr - g.xb) * NC * 2 * g.zp;
   fill_ghost_rows<<<grid_for(n2, 256), 256, 0, st>>>(g, NC, reinterpret_cast<uint32_t*>(buf));
   return cudaGetLastError();
 }

@@ -435,6 +435,19 @@ __device__ __forceinline__ void put_pair(const Geo& g, E* cell, E* plane_base, i
   }
 }
 
+// NaN-propagating min / max (PTX min.NaN / max.NaN): a NaN component makes the whole tree NaN,
+// so the saturation test below counts it (fminf / fmaxf would drop it), as pull_cells does
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 // store of one finished cell pair + fused statistics; z = logical z of the .x cell (even)
 template <bool Q16, bool DITHER, bool STATS, int QMODE>
 __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int q, int y, int z, int64_t cell_off0, bool statx,
@@ -488,14 +501,14 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
       // saturation counters: m outside [min, max]  (checked before the dither is added)
       bool satx, saty;
       if (B16) {   // every component maps [min, max] onto [0.5, 65535.5]: two min/max trees
-        const float lo0 = fminf(fminf(fminf(fminf(t[0].x, t[1].x), fminf(t[2].x, t[3].x)),
-                                      fminf(fminf(t[4].x, t[5].x), fminf(t[6].x, t[7].x))), fminf(t[8].x, t[9].x));
-        const float hi0 = fmaxf(fmaxf(fmaxf(fmaxf(t[0].x, t[1].x), fmaxf(t[2].x, t[3].x)),
-                                      fmaxf(fmaxf(t[4].x, t[5].x), fmaxf(t[6].x, t[7].x))), fmaxf(t[8].x, t[9].x));
-        const float lo1 = fminf(fminf(fminf(fminf(t[0].y, t[1].y), fminf(t[2].y, t[3].y)),
-                                      fminf(fminf(t[4].y, t[5].y), fminf(t[6].y, t[7].y))), fminf(t[8].y, t[9].y));
-        const float hi1 = fmaxf(fmaxf(fmaxf(fmaxf(t[0].y, t[1].y), fmaxf(t[2].y, t[3].y)),
-                                      fmaxf(fmaxf(t[4].y, t[5].y), fmaxf(t[6].y, t[7].y))), fmaxf(t[8].y, t[9].y));
+        const float lo0 = fmin_nan(fmin_nan(fmin_nan(fmin_nan(t[0].x, t[1].x), fmin_nan(t[2].x, t[3].x)),
+                                      fmin_nan(fmin_nan(t[4].x, t[5].x), fmin_nan(t[6].x, t[7].x))), fmin_nan(t[8].x, t[9].x));
+        const float hi0 = fmax_nan(fmax_nan(fmax_nan(fmax_nan(t[0].x, t[1].x), fmax_nan(t[2].x, t[3].x)),
+                                      fmax_nan(fmax_nan(t[4].x, t[5].x), fmax_nan(t[6].x, t[7].x))), fmax_nan(t[8].x, t[9].x));
+        const float lo1 = fmin_nan(fmin_nan(fmin_nan(fmin_nan(t[0].y, t[1].y), fmin_nan(t[2].y, t[3].y)),
+                                      fmin_nan(fmin_nan(t[4].y, t[5].y), fmin_nan(t[6].y, t[7].y))), fmin_nan(t[8].y, t[9].y));
+        const float hi1 = fmax_nan(fmax_nan(fmax_nan(fmax_nan(t[0].y, t[1].y), fmax_nan(t[2].y, t[3].y)),
+                                      fmax_nan(fmax_nan(t[4].y, t[5].y), fmax_nan(t[6].y, t[7].y))), fmax_nan(t[8].y, t[9].y));
         satx = statx && !(lo0 >= 0.5f && hi0 <= 65535.5f);   // NaN counts as saturated
         saty = staty && !(lo1 >= 0.5f && hi1 <= 65535.5f);
         if (satx || saty) {   // rare: per-component counts from the same t
@@ -511,8 +524,8 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
 #pragma unroll
         for (int c = 0; c < 10; ++c) {
           const V r = vfma(s[c], vsplat(A.Q.sat_a[c]), vsplat(A.Q.sat_b[c]));
-          mx0 = fmaxf(mx0, fabsf(r.x));
-          mx1 = fmaxf(mx1, fabsf(r.y));
+          mx0 = fmax_nan(mx0, fabsf(r.x));
+          mx1 = fmax_nan(mx1, fabsf(r.y));
         }
         satx = statx && !(mx0 <= 1.0f);
         saty = staty && !(mx1 <= 1.0f);

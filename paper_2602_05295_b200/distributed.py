@@ -7,7 +7,9 @@ rank sends its first and last interior x-planes (all components, including the y
 layers -- planes are contiguous in the state layout) into the neighbours' ghost planes.
 
 The exchange runs over ``torch.distributed`` point-to-point (NCCL over NVLink on the GPU
-box, gloo in the CPU tests).  Ranks at a non-periodic x face have no neighbour there; their
+box, gloo in the CPU tests).  With a gloo group and GPU slabs (several ranks sharing one GPU in
+the tests) the planes are staged through host memory: device -> host, gloo send/recv, host ->
+device, in stream order on the compute stream.  Ranks at a non-periodic x face have no neighbour there; their
 ghost plane is resolved by the BC inside the kernels (inflow constants / outflow clamp /
 wall bounce-back).
 
@@ -139,6 +141,8 @@ class DistributedSolver:
         self._comm_stream = None
         self._edge_stream = None
         self._comm_done = None
+        # gloo cannot move device tensors: stage the planes through host memory
+        self._staged = self._cuda and dist.get_backend(group) == "gloo"
         if self._cuda:
             # kernels run on torch's current stream; the halo exchange on its own stream
             self.solver.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -157,6 +161,14 @@ class DistributedSolver:
         """Blocking (stream-ordered on CUDA) exchange of the current -- or next -- buffer's
         edge planes into the neighbours' ghost planes."""
         t = self._halo_tensors(next_buffer)
+        if self._staged:
+            host = [x.cpu() for x in t[:2]] + [self._torch.empty_like(x, device="cpu") for x in t[2:]]
+            exchange_halos(host[0], host[1], host[2], host[3], self.plan, self.group)
+            if self.plan.lo is not None:
+                t[2].copy_(host[2])
+            if self.plan.hi is not None:
+                t[3].copy_(host[3])
+            return
         exchange_halos(t[0], t[1], t[2], t[3], self.plan, self.group)
 
     def _post_exchange_next(self, edges_done=None):
@@ -164,6 +176,11 @@ class DistributedSolver:
         (`edges_done`: the event after the edge kernels; default: now on the compute stream)."""
         torch = self._torch
         if not self._cuda:
+            self.exchange(next_buffer=True)
+            return
+        if self._staged:   # host-staged planes: in order on the compute stream
+            if edges_done is not None:
+                torch.cuda.current_stream().wait_event(edges_done)
             self.exchange(next_buffer=True)
             return
         if edges_done is None:
@@ -224,25 +241,46 @@ class DistributedSolver:
         self._synced_version = self._state_version()
 
     def step(self, n: int = 1, stats: bool = True):
+        """n steps on every rank; with ``stats`` the StepStats of the last step reduced over the
+        ranks.  Divergence on any rank raises FloatingPointError on every rank, after the
+        reduction (a local raise before it would leave the other ranks blocked in it)."""
         for k in range(n):
             self._one_step(stats and k == n - 1)
         if stats:
-            return self.reduce_stats(self.solver.read_stats())
+            try:
+                st = self.solver.read_stats(check=False)
+            except TypeError:          # injected slabs without the check flag
+                st = self.solver.read_stats()
+            return self.reduce_stats(st)
         return None
 
     def reduce_stats(self, st):
+        """Sum mass / momentum / n_fluid / saturation / force / torque, max of max|u| and of a
+        diverged flag (non-finite or |u| >= 0.9) over the ranks; raises
+        FloatingPointError on every rank when any rank diverged."""
         import torch
         import torch.distributed as dist
-        dev = "cuda" if self._cuda else "cpu"
-        v = torch.tensor([st.mass, *st.momentum, st.n_fluid, *st.saturation], dtype=torch.float64,
-                         device=dev)
+        dev = "cuda" if (self._cuda and not self._staged) else "cpu"
+        force = np.zeros(3) if st.force is None else np.asarray(st.force, dtype=np.float64)
+        torque = np.zeros(3) if st.torque is None else np.asarray(st.torque, dtype=np.float64)
+        finite = bool(getattr(st, "finite", True)) and np.isfinite(st.max_u) and np.isfinite(st.mass)
+        diverged = 0.0 if (finite and st.max_u < 0.9) else 1.0
+        v = torch.tensor([st.mass, *st.momentum, st.n_fluid, *st.saturation, *force, *torque],
+                         dtype=torch.float64, device=dev)
         dist.all_reduce(v, group=self.group)
-        m = torch.tensor([st.max_u], dtype=torch.float64, device=dev)
+        # NaN max|u| would poison a MAX reduction on some backends: send it as the flag + 1e300
+        m = torch.tensor([st.max_u if np.isfinite(st.max_u) else 1e300, diverged], dtype=torch.float64, device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
         v = v.cpu().numpy()
+        m = m.cpu().numpy()
         st.mass = float(v[0])
         st.momentum = v[1:4]
         st.n_fluid = int(v[4])
         st.saturation = v[5:15].astype(np.int64)
-        st.max_u = float(m.item())
+        st.force = v[15:18]
+        st.torque = v[18:21]
+        st.max_u = float(m[0])
+        if m[1] > 0:
+            raise FloatingPointError("solver divergence on at least one rank (non-finite moment or "
+                                     f"max |u| >= 0.9; global max |u| {st.max_u:.3g})")
         return st

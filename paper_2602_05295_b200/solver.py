@@ -113,6 +113,7 @@ class StepStats:
     n_fluid: int
     force: np.ndarray = None      # triangle mesh: momentum exchange on the solid
     torque: np.ndarray = None
+    finite: bool = True
 
     @classmethod
     def _from_c(cls, s: "_lib.HlbmStats") -> "StepStats":
@@ -120,7 +121,7 @@ class StepStats:
                    t_solid_ms=s.t_solid_ms, mass=s.mass, momentum=np.array(list(s.momentum)),
                    max_u=s.max_u, saturation=np.array(list(s.saturation), dtype=np.int64),
                    n_fluid=int(s.n_fluid), force=np.array(list(s.force)),
-                   torque=np.array(list(s.torque)))
+                   torque=np.array(list(s.torque)), finite=bool(s.finite))
 
 
 @dataclass
@@ -143,6 +144,7 @@ class Solver:
         self._lib = _lib.load()
         nx, ny, nz = grid.dims
         c = _lib.HlbmConfig()
+        self._lib.hlbm_config_init(C.byref(c))     # struct_size (ABI guard) + defaults
         c.nx, c.ny, c.nz = nx, ny, nz
         c.gnx = slab.gnx if slab else nx
         c.gny, c.gnz = ny, nz
@@ -278,9 +280,14 @@ class Solver:
         self.state_version += 1
         self._chk(self._lib.hlbm_step_async(self._ctx, int(n), int(with_stats)))
 
-    def read_stats(self) -> StepStats:
+    def read_stats(self, check: bool = True) -> StepStats:
+        """StepStats of the last step run with statistics.  ``check=False`` returns them even when
+        they report divergence (``finite`` False or max|u| >= 0.9) instead of raising, so that a
+        multi-rank caller can reduce a divergence flag before raising on every rank."""
         s = _lib.HlbmStats()
-        self._chk(self._lib.hlbm_read_stats(self._ctx, C.byref(s)))
+        rc = self._lib.hlbm_read_stats(self._ctx, C.byref(s))
+        if not (rc == _lib.HLBM_EDIVERGED and not check):
+            self._chk(rc)
         return StepStats._from_c(s)
 
     def step_fused(self, n: int = 1) -> StepStats:

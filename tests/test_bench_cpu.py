@@ -1,0 +1,66 @@
+"""bench.py host logic on CPU: the `--gpus N` self-launch under torchrun, the world-size check, and
+the reference arm's x-slab-with-halo step (it must equal the periodic single-domain step)."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+
+
+def test_self_launch_command():
+    cmd = bench.self_launch_cmd(["--gpus", "4", "--steps", "5"], 4, port=29555)
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[cmd.index("--master-port") + 1] == "29555"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"] and cmd[-5].endswith("bench.py")
+
+
+def test_world_check_fails_loudly():
+    bench.check_world(2, 2, 8)
+    with pytest.raises(SystemExit, match="WORLD_SIZE"):
+        bench.check_world(8, 1, 8)
+    with pytest.raises(SystemExit, match="visible"):
+        bench.check_world(8, 8, 1)
+
+
+def test_self_launch_spawns_n_ranks_reference_arm():
+    """`bench.py --impl reference --gpus 2` without a launcher runs two ranks under torchrun; rank 0
+    prints the single JSON line with n_gpus = 2, the other rank exits 0 without work."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["BENCH_REF_N"] = "16"
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    import json
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_xslab_reference_step_equals_periodic_step(tmp_path):
+    n, procs = 16, 4
+    paths = [str(tmp_path / f"s{b}") for b in range(2)]
+    for p in paths:
+        np.memmap(p, dtype=np.float64, mode="w+", shape=(10, n, n, n)).flush()
+    st = bench._initial_state(n)
+    a = np.memmap(paths[0], dtype=np.float64, mode="r+", shape=(10, n, n, n))
+    a[:] = st
+    a.flush()
+    bench._slab_init(paths, n)
+    bounds = np.linspace(0, n, procs + 1).astype(int)
+    for i in range(procs):
+        bench._slab_step((bounds[i], bounds[i + 1], 0))
+    got = np.asarray(bench._SLAB["bufs"][1])
+    kind, step, _ = bench._ref_modules()
+    r, m, s = step(st[0], st[1:4], st[4:10], bench.TAU)
+    np.testing.assert_allclose(got, np.concatenate([r[None], m, s]), rtol=0, atol=1e-15)

@@ -61,6 +61,7 @@ def test_create_without_gpu_fails_loudly():
     if lib.hlbm_device_count() > 0:
         pytest.skip("a GPU is visible")
     c = _lib.HlbmConfig()
+    lib.hlbm_config_init(C.byref(c))
     c.nx = c.ny = c.nz = 8
     c.tau = 0.6
     ctx = C.c_void_p()
@@ -75,6 +76,7 @@ def test_invalid_grid_rejected_by_the_library():
     import ctypes as C
     lib = _lib.load()
     c = _lib.HlbmConfig()
+    lib.hlbm_config_init(C.byref(c))
     c.nx, c.ny, c.nz = 8, 8, 6
     c.tau = 0.6
     ctx = C.c_void_p()
@@ -93,3 +95,44 @@ def test_lattice_choice_validation():
     assert SolverConfig(lattice="D3Q19").lattice == "D3Q19"
     with pytest.raises(ValueError):
         SolverConfig(lattice="D3Q15")
+
+
+def test_config_struct_size_guard():
+    """hlbm_config carries its own size: a binding built against another layout (the round-1
+    INTEGRATION.md struct without `q`, 8 bytes short) is rejected before any field is read."""
+    import ctypes as C
+    lib = _lib.load()
+    c = _lib.HlbmConfig()
+    lib.hlbm_config_init(C.byref(c))
+    assert c.struct_size == C.sizeof(_lib.HlbmConfig) == 352
+    assert c.q == 27 and list(c.bits) == [16] * 10 and c.qmax[0] == 1.5
+    c.nx = c.ny = c.nz = 8
+    c.tau = 0.6
+    c.struct_size = 344
+    ctx = C.c_void_p()
+    assert lib.hlbm_create(C.byref(c), C.byref(ctx)) == _lib.HLBM_EINVAL
+    assert b"struct_size is 344" in lib.hlbm_last_error(ctx)
+    lib.hlbm_destroy(ctx)
+
+
+def test_ctypes_layout_matches_the_c_header(tmp_path):
+    """Field offsets of the ctypes structs equal offsetof() of include/hlbm.h compiled by gcc."""
+    import ctypes as C
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "hlbm.h"', "int main(void){"]
+    for st, cname in ((_lib.HlbmConfig, "hlbm_config"), (_lib.HlbmStats, "hlbm_stats")):
+        src.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in st._fields_:
+            src.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src.append("return 0;}")
+    (tmp_path / "l.c").write_text("\n".join(src))
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(tmp_path / "l.c"), "-o", str(tmp_path / "l")], check=True)
+    got = subprocess.run([str(tmp_path / "l")], capture_output=True, text=True, check=True).stdout.split("\n")
+    want = []
+    for st, cname in ((_lib.HlbmConfig, "hlbm_config"), (_lib.HlbmStats, "hlbm_stats")):
+        want.append(f"{cname} size {C.sizeof(st)}")
+        want += [f"{cname} {f} {getattr(st, f).offset}" for f, _ in st._fields_]
+    assert [g for g in got if g] == want
