@@ -127,9 +127,17 @@ int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats);
 int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out);
 /* full-grid update with the per-cell pull kernel (GPU reference for the fast kernel) */
 int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps);
-/* the original fused HOME-LBM step (Alg. 1): one kernel, one thread per
- * cell, 27-link pull with voxel solid links resolved inline (bounce-back, solid cells at rest);
- * the in-repo baseline of the split-scheme attribution.  Voxel solids only. */
+/* per-cell gather step: one thread per cell of the slab pulls its 27 (19) sources, each
+ * re-evaluating the source's collision and reconstruction, voxel solid links inline; the same
+ * Alg.-2 storage cut as hlbm_step (the GPU cross-check of the split kernels, and the D3Q19 path of
+ * non-default codecs).  Voxel solids only. */
+int hlbm_step_percell(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
+/* the original HOME-LBM step (Alg. 1): the stored state is the
+ * POST-collision moments; each node reconstructs its own populations into shared memory (8^3
+ * tiles + halo), streams from its neighbours there (solid links: bounce-back inline), extracts,
+ * collides and writes back.  The in-repo baseline of the split-scheme attribution
+ * (PAPER.md:418-429).  Related to hlbm_step by the half-step alignment (S o C)^n o S = S o (C o S)^n
+ * (SPEC.md:495).  Voxel solids only, single domain. */
 int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
 
 /* boundary list: global linear cell indices (sorted) and link masks; cells==NULL -> count only */

@@ -142,7 +142,7 @@ def solid_cells(mask):
 
 # ---------------------------------------------------------------- the step
 
-def step_padded(padded, tau, force=None, link_solid=None, lat=None):
+def step_padded(padded, tau, force=None, link_solid=None, lat=None, collide=True):
     """One Alg.-2 update of a ghost-padded 10-component block.
 
     ``padded`` is (10, nx+2, ny+2, nz+2) in (rho, mom, stress) form; returns
@@ -151,7 +151,10 @@ def step_padded(padded, tau, force=None, link_solid=None, lat=None):
     direction i is solid (half-way bounce-back replaces that population)."""
     lat = lat or L.D3Q27
     rho, mom, stress = padded[0], padded[1:4], padded[4:10]
-    r, m, s = collide_moments(rho, mom, stress, force, tau)       # collision.py:137
+    if collide:
+        r, m, s = collide_moments(rho, mom, stress, force, tau)   # collision.py:137
+    else:                                                         # streaming S alone (Alg.-1 cut)
+        r, m, s = rho, mom, stress
     f = reconstruct_distributions(r, m, s, lat)                     # moments.py:64
     nx, ny, nz = (d - 2 for d in rho.shape)
     fs = np.empty((lat.Q, nx, ny, nz))
@@ -168,8 +171,9 @@ def step_padded(padded, tau, force=None, link_solid=None, lat=None):
     return moments_from_distributions(fs, lat)                      # moments.py:25
 
 
-def fluid_step(rho, mom, stress, tau, bc: BC | None = None, force=None, mask=None, lat=None):
-    """One fluid update of the whole grid in the reference layout (``lat``: D3Q27 default)."""
+def fluid_step(rho, mom, stress, tau, bc: BC | None = None, force=None, mask=None, lat=None, collide=True):
+    """One fluid update of the whole grid in the reference layout (``lat``: D3Q27 default);
+    ``collide=False`` applies the streaming operator alone (``stream_step``)."""
     bc = bc or BC()
     lat = lat or L.D3Q27
     padded = pad_state(rho, mom, stress, bc)
@@ -181,12 +185,32 @@ def fluid_step(rho, mom, stress, tau, bc: BC | None = None, force=None, mask=Non
         link_solid = ((lm[None] >> np.arange(lat.Q, dtype=np.uint32)[:, None, None, None])
                       & np.uint32(1)).astype(bool)
         solid = mask
-    r, m, s = step_padded(padded, tau, force, link_solid, lat)
+    r, m, s = step_padded(padded, tau, force, link_solid, lat, collide)
     if solid is not None and solid.any():
         r[solid] = 1.0
         m[:, solid] = 0.0
         s[:, solid] = 0.0
     return r, m, s
+
+
+def stream_step(rho, mom, stress, bc: BC | None = None, mask=None, lat=None):
+    """The streaming operator S alone: reconstruct the stored moments (moments.py:64-90), pull-stream
+    with the same BC / bounce-back rules as ``fluid_step``, extract (moments.py:25-39); solid cells
+    at rest.  A split step is S o C and an Alg.-1 step is C o S, so
+    (S o C)^n o S = S o (C o S)^n relates the two storage cuts."""
+    return fluid_step(rho, mom, stress, 1.0, bc, None, mask, lat, collide=False)
+
+
+def alg1_step(rho, mom, stress, tau, bc: BC | None = None, force=None, mask=None, lat=None):
+    """One original HOME-LBM step (Alg. 1) on post-collision moments: C o S."""
+    r, m, s = stream_step(rho, mom, stress, bc, mask, lat)
+    r2, m2, s2 = collide_moments(r, m, s, force, tau)
+    if mask is not None and np.any(mask):
+        sol = np.asarray(mask, dtype=bool)
+        r2[sol] = 1.0
+        m2[:, sol] = 0.0
+        s2[:, sol] = 0.0
+    return r2, m2, s2
 
 
 def _has_wall(bc: BC):

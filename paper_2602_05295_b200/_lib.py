@@ -69,6 +69,7 @@ SIGNATURES = {
     "hlbm_read_stats": (C.c_int, [_P, C.POINTER(HlbmStats)]),
     "hlbm_step_reference": (C.c_int, [_P, C.c_int32]),
     "hlbm_step_fused": (C.c_int, [_P, C.c_int32, C.POINTER(HlbmStats)]),
+    "hlbm_step_percell": (C.c_int, [_P, C.c_int32, C.POINTER(HlbmStats)]),
     "hlbm_get_boundary": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_int64)]),
     "hlbm_get_codes": (C.c_int, [_P, C.POINTER(C.c_uint32)]),

@@ -874,9 +874,9 @@ int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
   return HLBM_OK;
 }
 
-int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
+int hlbm_step_percell(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
-  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the fused step supports voxel solids only");
+  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the per-cell step supports voxel solids only");
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
   float tf = 0.f;
@@ -888,6 +888,40 @@ int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     CK(launch_pull_cells(A, nullptr, ctx->d_fused, n, 3, q16, force, dither, ctx->stream, ctx->q));
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     ++ctx->launches;
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    float a = 0.f;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    tf += a;
+    ctx->cur = 1 - ctx->cur;
+    ++ctx->steps;
+  }
+  if (nsteps == 0) return HLBM_OK;
+  ctx->last_t_fluid = tf / nsteps;
+  ctx->last_t_solid = 0.0;
+  return hlbm_read_stats(ctx, out);
+}
+
+// the original HOME-LBM step (Alg. 1): post-collision storage cut, 8^3 tiles with
+// shared-memory streaming, voxel solid links inline (hlbm_cells.cu alg1_step)
+int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
+  if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the fused Alg.-1 step supports voxel solids only");
+  if (ctx->cfg.x_lo_remote || ctx->cfg.x_hi_remote)
+    return fail(ctx, HLBM_EINVAL, "the fused Alg.-1 step runs on a single domain");
+  const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
+  float tf = 0.f;
+  for (int s = 0; s < nsteps; ++s) {
+    const int st = (s == nsteps - 1) ? 1 : 0;
+    if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+    StepArgs A = make_args(ctx, st);
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    CK(launch_alg1(A, ctx->d_fused, q16, force, dither, ctx->q, ctx->stream));
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    ++ctx->launches;
+    if (ctx->cfg.ny == 1) {   // one-row slab: both ghost rows hold the edge row's image
+      CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], ctx->stream));
+      ++ctx->launches;
+    }
     CK(cudaEventSynchronize(ctx->ev[1]));
     float a = 0.f;
     cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);

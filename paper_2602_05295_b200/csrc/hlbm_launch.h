@@ -41,6 +41,10 @@ cudaError_t launch_fluid_interior19(const StepArgs& A, bool q16, bool force, boo
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither, cudaStream_t st,
                               int q = 27, int64_t base = 0);
+// original HOME-LBM step (Alg. 1): post-collision storage cut, own-population
+// reconstruction into shared memory, streaming within 8^3 tiles, voxel solid links inline
+cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool force, bool dither, int q,
+                        cudaStream_t st);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
                           const double* mom, const double* stress, int x0, int cnt,
                           unsigned long long* sat, cudaStream_t st);

@@ -142,7 +142,7 @@ class DistributedSolver:
         self._edge_stream = None
         self._comm_done = None
         # gloo cannot move device tensors: stage the planes through host memory
-        self._staged = self._cuda and dist.get_backend(group) == "gloo"
+        self._staged = self._cuda and dist.is_initialized() and dist.get_backend(group) == "gloo"
         if self._cuda:
             # kernels run on torch's current stream; the halo exchange on its own stream
             self.solver.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -265,6 +265,10 @@ class DistributedSolver:
         torque = np.zeros(3) if st.torque is None else np.asarray(st.torque, dtype=np.float64)
         finite = bool(getattr(st, "finite", True)) and np.isfinite(st.max_u) and np.isfinite(st.mass)
         diverged = 0.0 if (finite and st.max_u < 0.9) else 1.0
+        if not dist.is_initialized():      # a single rank without a process group
+            if diverged:
+                raise FloatingPointError(f"solver divergence (max |u| {st.max_u:.3g} or non-finite moment)")
+            return st
         v = torch.tensor([st.mass, *st.momentum, st.n_fluid, *st.saturation, *force, *torque],
                          dtype=torch.float64, device=dev)
         dist.all_reduce(v, group=self.group)

@@ -291,11 +291,23 @@ class Solver:
         return StepStats._from_c(s)
 
     def step_fused(self, n: int = 1) -> StepStats:
-        """The original fused HOME-LBM step (Alg. 1): one kernel, one thread per cell,
-        solid links resolved inline -- the in-repo baseline of the split scheme (voxel solids)."""
+        """The original HOME-LBM step (Alg. 1, SPEC.md `fused_step`): the stored state is
+        read as POST-collision moments (Alg. 1's storage cut); per node reconstruct own f, stream
+        through shared memory (8^3 tiles), solid links inline, extract, collide, write back.  n steps
+        of it from m0 followed by one streaming S equal n split steps from S(m0).
+        The in-repo baseline of the split scheme (voxel solids, single domain)."""
         self.state_version += 1
         s = _lib.HlbmStats()
         self._chk(self._lib.hlbm_step_fused(self._ctx, int(n), C.byref(s)))
+        self._last = StepStats._from_c(s)
+        return self._last
+
+    def step_percell(self, n: int = 1) -> StepStats:
+        """Per-cell gather step with the same storage cut as ``step`` (one thread per cell pulls its
+        sources, each re-evaluating the source's collision): the GPU cross-check of the split kernels."""
+        self.state_version += 1
+        s = _lib.HlbmStats()
+        self._chk(self._lib.hlbm_step_percell(self._ctx, int(n), C.byref(s)))
         self._last = StepStats._from_c(s)
         return self._last
 

@@ -228,8 +228,8 @@ def test_q16_saturation_counts():
 
 
 @pytest.mark.parametrize("bcname", ["channel", "closed"])
-def test_fused_alg1_step_matches_oracle_and_split(bcname):
-    """The fused single-kernel step (Alg. 1 baseline, solid links inline) against the
+def test_percell_step_matches_oracle_and_split(bcname):
+    """The per-cell gather step (one kernel, solid links inline, same storage cut) against the
     oracle (fp32 tolerance) and against the split scheme (interior kernel + compacted boundary
     kernel): the two schemes compute the same step."""
     shape = (40, 24, 28)
@@ -245,7 +245,7 @@ def test_fused_alg1_step_matches_oracle_and_split(bcname):
     for scheme in ("fused", "split"):
         with Solver(SimGrid(shape, mask), cfg) as s:
             s.set_moments(*state)
-            st = s.step_fused(5) if scheme == "fused" else s.step(5)
+            st = s.step_percell(5) if scheme == "fused" else s.step(5)
             res[scheme] = (s.moments(), st)
     ref = state
     for _ in range(5):
@@ -257,7 +257,7 @@ def test_fused_alg1_step_matches_oracle_and_split(bcname):
     assert res["fused"][1].mass == pytest.approx(res["split"][1].mass, rel=1e-7)
 
 
-def test_fused_alg1_q16_matches_split_within_1_lsb():
+def test_percell_q16_matches_split_within_1_lsb():
     shape = (32, 20, 24)
     mask = sphere_mask(shape, (12, 9.5, 11.5), 4)
     bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("periodic", "periodic")}
@@ -268,7 +268,7 @@ def test_fused_alg1_q16_matches_split_within_1_lsb():
         with Solver(SimGrid(shape, mask), cfg) as s:
             s.set_moments(*state)
             if scheme == "fused":
-                s.step_fused(1)
+                s.step_percell(1)
             else:
                 s.step(1)
             words[scheme] = s.codes
@@ -332,7 +332,7 @@ def test_d3q19_q16_within_1_lsb():
 def test_d3q19_interior_kernel_matches_per_cell(precision, bcname):
     """D3Q19 steps run the interior kernel with two-chain streaming (216 w = prod(4,1,1) +
     prod(2,-1,-1)) plus the compacted 19-link kernels for solids; they match the per-cell D3Q19
-    kernel (step_fused) and the oracle: fp32 per-moment relative error <= 1e-5, q16 codes within
+    kernel (step_percell) and the oracle: fp32 per-moment relative error <= 1e-5, q16 codes within
     1 LSB."""
     from oracle import lattice as OL
     shape = (20, 33, 68)   # ragged tiles in y and z
@@ -351,7 +351,7 @@ def test_d3q19_interior_kernel_matches_per_cell(precision, bcname):
                 s.codes = codec.encode_state(state[0], state[1], neq_decompose(*state))[0]
             else:
                 s.set_moments(*state)
-            s.step(2) if kind == "interior" else s.step_fused(2)
+            s.step(2) if kind == "interior" else s.step_percell(2)
             res[kind] = s.codes if precision == "q16" else s.moments()
     if precision == "q16":
         d = np.abs(codec.unpack(res["interior"]).astype(np.int64) - codec.unpack(res["per_cell"]).astype(np.int64))
@@ -373,7 +373,7 @@ def test_tiny_and_ragged_grids(shape, kernel):
     cfg = SolverConfig(nu=0.02)
     with Solver(SimGrid(shape), cfg) as s:
         s.set_moments(*state)
-        s.step(2) if kernel == "split" else s.step_fused(2)
+        s.step(2) if kernel == "split" else s.step_percell(2)
         got = s.moments()
     ref = OS.run(*state, cfg.tau, 2)
     err = moment_errors(got, ref)

