@@ -122,6 +122,18 @@ int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmo
  * compacted boundary/solid kernel; blocks until done and fills *out (may be NULL). Returns
  * HLBM_EDIVERGED when max|u| >= 0.9 or a non-finite value appeared. */
 int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
+/* SPEC's split step as two calls (Alg. 2 / Alg. 3 roles):
+ * hlbm_fluid_update runs the interior kernel over every cell (no obstacle logic); with obstacles the
+ * step stays uncommitted until hlbm_solid_correction runs the compacted boundary / solid / cut-link
+ * kernels on the same output buffer (any other state access runs it implicitly).  Without
+ * obstacles hlbm_fluid_update commits the step and hlbm_solid_correction is the identity.
+ * hlbm_solid_correction fills *out (may be NULL) with the step's StepStats and phase times. */
+int hlbm_fluid_update(hlbm_ctx* ctx, int32_t with_stats);
+int hlbm_solid_correction(hlbm_ctx* ctx, hlbm_stats* out);
+/* the streaming operator S alone (reconstruct the stored moments, pull-stream with the BC and
+ * voxel bounce-back rules, extract; no collision): converts an Alg.-1 state (post-collision) to
+ * the split scheme's storage cut, (S o C)^n o S = S o (C o S)^n.  Not a time step. */
+int hlbm_stream(hlbm_ctx* ctx);
 /* the same launches, enqueued on the context stream without synchronising */
 int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats);
 int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out);

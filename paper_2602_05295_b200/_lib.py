@@ -66,6 +66,9 @@ SIGNATURES = {
     "hlbm_init_modes": (C.c_int, [_P, C.c_double, _DP, C.c_int32]),
     "hlbm_step": (C.c_int, [_P, C.c_int32, C.POINTER(HlbmStats)]),
     "hlbm_step_async": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "hlbm_fluid_update": (C.c_int, [_P, C.c_int32]),
+    "hlbm_solid_correction": (C.c_int, [_P, C.POINTER(HlbmStats)]),
+    "hlbm_stream": (C.c_int, [_P]),
     "hlbm_read_stats": (C.c_int, [_P, C.POINTER(HlbmStats)]),
     "hlbm_step_reference": (C.c_int, [_P, C.c_int32]),
     "hlbm_step_fused": (C.c_int, [_P, C.c_int32, C.POINTER(HlbmStats)]),

@@ -53,6 +53,7 @@ struct hlbm_ctx {
   float solid_v[3] = {0, 0, 0}, solid_w[3] = {0, 0, 0}, solid_c[3] = {0, 0, 0};
   std::vector<int64_t> off_b, off_s, off_m;   // per-plane offsets (nx+1) into the sorted lists
   int pending_stats = 0;                      // statistics requested for the step in progress
+  int pending_solid = 0;                      // hlbm_fluid_update ran, its solid correction not yet
   int64_t steps = 0;
   int64_t launches = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -217,9 +218,12 @@ int fix_one_row(hlbm_ctx* ctx, int xb, int xr, cudaStream_t st) {
 }
 
 // interior kernel + compacted boundary kernels for destination planes [xb, xr), on stream st
-// (default: the context's stream)
+// (default: the context's stream).  phases: bit 0 the fluid update (interior kernel, every cell,
+// no obstacle logic), bit 1 the solid correction (compacted kernels over the boundary / solid /
+// cut-link lists, which overwrite their cells of the same output buffer)
+constexpr int kPhaseFluid = 1, kPhaseSolid = 2;
 int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_interior = nullptr,
-              cudaStream_t st = nullptr) {
+              cudaStream_t st = nullptr, int phases = kPhaseFluid | kPhaseSolid) {
   if (xr <= xb) return HLBM_OK;
   if (!st) st = ctx->stream;
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
@@ -228,7 +232,8 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   const bool fast19 = ctx->q == 19 && (!q16 || ctx->qmode == 2);
   if (ctx->q == 19 && !fast19) {
     // D3Q19 with a non-default codec: the per-cell fused kernel over the planes of the range,
-    // solid links inline
+    // solid links inline (no separate correction phase)
+    if (!(phases & kPhaseFluid)) return HLBM_OK;
     const int64_t pl = (int64_t)ctx->cfg.ny * ctx->cfg.nz;
     CK(launch_pull_cells(A, nullptr, ctx->d_fused, (int64_t)(xr - xb) * pl, 3, q16, force, dither, st, 19,
                          (int64_t)xb * pl));
@@ -236,12 +241,15 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
     if (after_interior) CK(cudaEventRecord(after_interior, st));
     return fix_one_row(ctx, xb, xr, st);
   }
-  if (fast19)   // D3Q19: two-chain streaming; solids through the compacted 19-link kernels below
-    CK(launch_fluid_interior19(A, q16, force, special, dither, st));
-  else
-    CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, st));
-  ++ctx->launches;
+  if (phases & kPhaseFluid) {
+    if (fast19)   // D3Q19: two-chain streaming; solids through the compacted 19-link kernels below
+      CK(launch_fluid_interior19(A, q16, force, special, dither, st));
+    else
+      CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, st));
+    ++ctx->launches;
+  }
   if (after_interior) CK(cudaEventRecord(after_interior, st));
+  if (!(phases & kPhaseSolid)) return fix_one_row(ctx, xb, xr, st);
   auto sub = [&](const std::vector<int64_t>& off, int64_t n, int64_t& a, int64_t& cnt) {
     if (off.empty()) { a = 0; cnt = (xb == 0 && xr == ctx->cfg.nx) ? n : 0; return; }
     a = off[(size_t)xb];
@@ -269,6 +277,18 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
 }
 
 }  // namespace
+
+// SPEC's two-phase step (fluid_update_step then solid_correction_step): a fluid
+// update whose solid correction has not run yet leaves the step uncommitted (the corrected cells
+// of the output buffer are still missing); every other state access finishes it first
+static int settle(hlbm_ctx* ctx) {
+  if (!ctx || !ctx->pending_solid) return HLBM_OK;
+  return hlbm_solid_correction(ctx, nullptr);
+}
+#define SETTLE(ctx)                               \
+  do {                                            \
+    if (int r_ = settle(ctx)) return r_;          \
+  } while (0)
 
 extern "C" {
 
@@ -467,6 +487,7 @@ int64_t hlbm_launch_count(const hlbm_ctx* ctx) { return ctx ? ctx->launches : -1
 
 int hlbm_state_buffer(hlbm_ctx* ctx, void** ptr, int64_t* bytes) {
   if (!ctx) return HLBM_EINVAL;
+  SETTLE(ctx);
   if (ptr) *ptr = ctx->buf[ctx->cur];
   if (bytes) *bytes = ctx->total_elems * 4;
   return HLBM_OK;
@@ -475,6 +496,7 @@ int hlbm_state_buffer(hlbm_ctx* ctx, void** ptr, int64_t* bytes) {
 int hlbm_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
                      int64_t* bytes) {
   if (!ctx) return HLBM_EINVAL;
+  SETTLE(ctx);
   char* b = (char*)ctx->buf[ctx->cur];
   const int64_t pb = ctx->plane_elems * 4;
   if (send_lo) *send_lo = b + 1 * pb;
@@ -500,6 +522,7 @@ int hlbm_next_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** 
 
 int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const double* stress) {
   if (!ctx || !rho || !mom || !stress) return fail(ctx, HLBM_EINVAL, "null argument");
+  SETTLE(ctx);
   const hlbm_config& c = ctx->cfg;
   const int64_t n = (int64_t)c.nx * c.ny * c.nz;
   for (int64_t i = 0; i < n; ++i)
@@ -535,6 +558,7 @@ int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const 
 int hlbm_get_moments_box(hlbm_ctx* ctx, int32_t x0, int32_t cx, int32_t y0, int32_t cy, int32_t z0,
                          int32_t cz, double* rho, double* mom, double* stress) {
   if (!ctx || !rho || !mom || !stress) return fail(ctx, HLBM_EINVAL, "null argument");
+  SETTLE(ctx);
   const hlbm_config& c = ctx->cfg;
   if (x0 < 0 || cx < 0 || x0 + cx > c.nx || cy < 0 || cz < 0) return fail(ctx, HLBM_EINVAL, "box out of range");
   const int64_t pl = (int64_t)cy * cz;
@@ -571,6 +595,7 @@ int hlbm_get_moments(hlbm_ctx* ctx, double* rho, double* mom, double* stress) {
 
 int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmodes) {
   if (!ctx || (nmodes > 0 && !modes) || nmodes < 0) return fail(ctx, HLBM_EINVAL, "bad modes");
+  SETTLE(ctx);
   if (!(rho0 > 0.0)) return fail(ctx, HLBM_EINVAL, "density must be positive");
   double* dmodes = nullptr;
   if (nmodes > 0) {
@@ -610,6 +635,7 @@ static int copy_dense(hlbm_ctx* ctx, void* host, bool to_host) {
 
 int hlbm_get_state(hlbm_ctx* ctx, void* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
+  SETTLE(ctx);
   if (int r = copy_dense(ctx, words, true)) return r;
   CK(cudaStreamSynchronize(ctx->stream));
   return HLBM_OK;
@@ -617,6 +643,7 @@ int hlbm_get_state(hlbm_ctx* ctx, void* words) {
 
 int hlbm_set_state(hlbm_ctx* ctx, const void* words) {
   if (!ctx || !words) return fail(ctx, HLBM_EINVAL, "null argument");
+  SETTLE(ctx);
   if (int r = copy_dense(ctx, const_cast<void*>(words), false)) return r;
   CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[ctx->cur], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -643,6 +670,7 @@ int hlbm_set_codes(hlbm_ctx* ctx, const uint32_t* words) {
 
 int hlbm_set_mask(hlbm_ctx* ctx, const uint8_t* mask, const uint8_t* ghost_lo, const uint8_t* ghost_hi) {
   if (!ctx || !mask) return fail(ctx, HLBM_EINVAL, "null mask");
+  SETTLE(ctx);
   const hlbm_config& c = ctx->cfg;
   const int64_t pl = (int64_t)c.ny * c.nz, n = pl * c.nx;
   // planes -1 .. nx of the padded mask along x (oracle/step.py:padded_solid)
@@ -810,8 +838,71 @@ int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n
   return HLBM_OK;
 }
 
+int hlbm_fluid_update(hlbm_ctx* ctx, int32_t with_stats) {
+  if (!ctx) return HLBM_EINVAL;
+  SETTLE(ctx);
+  if (with_stats) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (int r = run_range(ctx, 0, ctx->cfg.nx, with_stats, ctx->ev[1], nullptr, kPhaseFluid)) return r;
+  ctx->pending_stats = with_stats ? 1 : 0;
+  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0 && !(ctx->q == 19 && ctx->q16 && ctx->qmode != 2);
+  if (special) {
+    ctx->pending_solid = 1;
+    return HLBM_OK;
+  }
+  CK(cudaEventRecord(ctx->ev[2], ctx->stream));   // no obstacles: the step is complete
+  ctx->cur = 1 - ctx->cur;
+  ++ctx->steps;
+  ctx->pending_stats = 0;
+  return HLBM_OK;
+}
+
+int hlbm_solid_correction(hlbm_ctx* ctx, hlbm_stats* out) {
+  if (!ctx) return HLBM_EINVAL;
+  if (ctx->pending_solid) {
+    if (int r = run_range(ctx, 0, ctx->cfg.nx, ctx->pending_stats, nullptr, nullptr, kPhaseSolid)) return r;
+    CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    ctx->pending_solid = 0;
+    ctx->cur = 1 - ctx->cur;
+    ++ctx->steps;
+  }
+  if (!out) return HLBM_OK;
+  const int had_stats = ctx->pending_stats;
+  ctx->pending_stats = 0;
+  CK(cudaStreamSynchronize(ctx->stream));
+  float a = 0.f, b = 0.f;
+  cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+  ctx->last_t_fluid = a;
+  ctx->last_t_solid = b;
+  if (!had_stats) {
+    memset(out, 0, sizeof(*out));
+    out->step = ctx->steps;
+    out->t_fluid_ms = a;
+    out->t_solid_ms = b;
+    out->finite = 1;
+    return HLBM_OK;
+  }
+  return hlbm_read_stats(ctx, out);
+}
+
+int hlbm_stream(hlbm_ctx* ctx) {
+  if (!ctx) return HLBM_EINVAL;
+  SETTLE(ctx);
+  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the streaming operator supports voxel solids only");
+  if (ctx->cfg.x_lo_remote || ctx->cfg.x_hi_remote) return fail(ctx, HLBM_EINVAL, "single domain only");
+  StepArgs A = make_args(ctx, 0);
+  CK(launch_alg1(A, ctx->d_fused, ctx->q16, false, ctx->q16 && ctx->cfg.dither, ctx->q, ctx->stream, false));
+  ++ctx->launches;
+  if (ctx->cfg.ny == 1) CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->cur = 1 - ctx->cur;
+  return HLBM_OK;
+}
+
 int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  SETTLE(ctx);
   for (int s = 0; s < nsteps; ++s) {
     const int st = (with_stats && s == nsteps - 1) ? 1 : 0;
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
@@ -824,6 +915,7 @@ int hlbm_step_async(hlbm_ctx* ctx, int32_t nsteps, int32_t with_stats) {
 
 int hlbm_step_begin(hlbm_ctx* ctx, int32_t with_stats) {
   if (!ctx) return HLBM_EINVAL;
+  SETTLE(ctx);
   ctx->pending_stats = with_stats ? 1 : 0;
   if (with_stats) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
   return HLBM_OK;
@@ -849,6 +941,7 @@ int hlbm_step_end(hlbm_ctx* ctx) {
 
 int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  SETTLE(ctx);
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
   for (int s = 0; s < nsteps; ++s) {
@@ -876,6 +969,7 @@ int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
 
 int hlbm_step_percell(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  SETTLE(ctx);
   if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the per-cell step supports voxel solids only");
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
@@ -905,6 +999,7 @@ int hlbm_step_percell(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
 // shared-memory streaming, voxel solid links inline (hlbm_cells.cu alg1_step)
 int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  SETTLE(ctx);
   if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the fused Alg.-1 step supports voxel solids only");
   if (ctx->cfg.x_lo_remote || ctx->cfg.x_hi_remote)
     return fail(ctx, HLBM_EINVAL, "the fused Alg.-1 step runs on a single domain");
@@ -915,7 +1010,7 @@ int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    CK(launch_alg1(A, ctx->d_fused, q16, force, dither, ctx->q, ctx->stream));
+    CK(launch_alg1(A, ctx->d_fused, q16, force, dither, ctx->q, ctx->stream, true));
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     ++ctx->launches;
     if (ctx->cfg.ny == 1) {   // one-row slab: both ghost rows hold the edge row's image
@@ -975,6 +1070,7 @@ int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {
 // One host synchronisation per call: the stats copy is enqueued behind the last kernel.
 int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  SETTLE(ctx);
   if (nsteps == 0) {
     if (out) { memset(out, 0, sizeof(*out)); out->step = ctx->steps; out->finite = 1; }
     return HLBM_OK;

@@ -320,7 +320,7 @@ struct GatherAll<Q, Q> {
   __device__ __forceinline__ static void run(const float*, int, uint32_t, float*) {}
 };
 
-template <bool Q16, bool FORCE, bool DITHER, int Q>
+template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE>
 __global__ void __launch_bounds__(kA1 * kA1 * kA1, 2) alg1_step(const __grid_constant__ StepArgs A,
                                                                 const uint32_t* __restrict__ fmask) {
   extern __shared__ float fsm[];   // [Q][kA1N]
@@ -367,38 +367,51 @@ __global__ void __launch_bounds__(kA1 * kA1 * kA1, 2) alg1_step(const __grid_con
       GatherAll<0, Q>::run(fsm, own, mask, m);
       float pre[10];
       raw_to_state<float>(m, pre);
+      if (!COLLIDE) {   // the streaming operator S alone (hlbm_stream)
+#pragma unroll
+        for (int c = 0; c < 10; ++c) s[c] = pre[c];
+      } else {
       const Post<float> P = collide<float, FORCE>(pre[0], pre[1], pre[2], pre[3], pre[4], pre[5], pre[6], pre[7],
                                                   pre[8], pre[9], A.R);
       s[0] = P.d; s[1] = P.jpx; s[2] = P.jpy; s[3] = P.jpz;
       s[4] = P.Xxx - P.jpx * P.ux; s[5] = P.Xxy - P.jpx * P.uy; s[6] = P.Xxz - P.jpx * P.uz;
       s[7] = P.Xyy - P.jpy * P.uy; s[8] = P.Xyz - P.jpy * P.uz; s[9] = P.Xzz - P.jpz * P.uz;
+      }
     }
     store_cell<Q16, DITHER>(A, x, y, z, s, A.do_stats && !(mask & 1u), red);
   }
   if (A.do_stats) flush_stats(A, red);
 }
 
-template <bool Q16, bool FORCE, bool DITHER, int Q>
+template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE>
 static cudaError_t launch_alg1_t(const StepArgs& A, const uint32_t* fmask, cudaStream_t st) {
   const Geo& g = A.g;
   const int64_t tiles = (int64_t)((g.nx + kA1 - 1) / kA1) * ((g.ny + kA1 - 1) / kA1) * ((g.nz + kA1 - 1) / kA1);
   const int smem = Q * kA1N * (int)sizeof(float);
   static bool attr = false;   // once per instantiation (not on every launch)
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(alg1_step<Q16, FORCE, DITHER, Q>,
+    cudaError_t e = cudaFuncSetAttribute(alg1_step<Q16, FORCE, DITHER, Q, COLLIDE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  alg1_step<Q16, FORCE, DITHER, Q><<<(unsigned)tiles, kA1 * kA1 * kA1, smem, st>>>(A, fmask);
+  alg1_step<Q16, FORCE, DITHER, Q, COLLIDE><<<(unsigned)tiles, kA1 * kA1 * kA1, smem, st>>>(A, fmask);
   return cudaGetLastError();
 }
 
 cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool force, bool dither, int q,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool collide) {
+  if (!collide) {   // S alone: no force term
+    if (q16) return dither ? (q == 19 ? launch_alg1_t<true, false, true, 19, false>(A, fmask, st)
+                                      : launch_alg1_t<true, false, true, 27, false>(A, fmask, st))
+                           : (q == 19 ? launch_alg1_t<true, false, false, 19, false>(A, fmask, st)
+                                      : launch_alg1_t<true, false, false, 27, false>(A, fmask, st));
+    return q == 19 ? launch_alg1_t<false, false, false, 19, false>(A, fmask, st)
+                   : launch_alg1_t<false, false, false, 27, false>(A, fmask, st);
+  }
 #define HLBM_A1(QQ, F, D)                                                          \
   if (q16 == QQ && force == F && dither == D)                                     \
-    return q == 19 ? launch_alg1_t<QQ, F, D, 19>(A, fmask, st) : launch_alg1_t<QQ, F, D, 27>(A, fmask, st);
+    return q == 19 ? launch_alg1_t<QQ, F, D, 19, true>(A, fmask, st) : launch_alg1_t<QQ, F, D, 27, true>(A, fmask, st);
   HLBM_A1(false, false, false)
   HLBM_A1(false, true, false)
   HLBM_A1(true, false, false)

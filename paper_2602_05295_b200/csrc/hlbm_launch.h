@@ -44,7 +44,7 @@ cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uin
 // original HOME-LBM step (Alg. 1): post-collision storage cut, own-population
 // reconstruction into shared memory, streaming within 8^3 tiles, voxel solid links inline
 cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool force, bool dither, int q,
-                        cudaStream_t st);
+                        cudaStream_t st, bool collide);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
                           const double* mom, const double* stress, int x0, int cnt,
                           unsigned long long* sat, cudaStream_t st);

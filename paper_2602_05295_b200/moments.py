@@ -1,7 +1,8 @@
 """Per-node moment value type returned by ``Solver.moment_set`` (host-side accessor).
 
-Mirrors ``MomentSet`` of the reference (moments.py:136-172): validation raises
-ValueError for rho <= 0 or |u_a| >= 1; ``velocity``; ``decompose`` (moments.py:93-96).
+The reference's own ``MomentSet`` (momentlbm/moments.py:136-172) when the reference package is
+importable; otherwise a stand-in with the same fields, validation (ValueError for rho <= 0 or
+|u_a| >= 1), ``velocity`` and ``decompose`` (moments.py:93-96).
 """
 
 from __future__ import annotations
@@ -14,7 +15,7 @@ _VOIGT_PAIRS = ((0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2))
 
 
 @dataclass
-class MomentSet:
+class _MomentSet:
     rho: float
     mom: np.ndarray
     stress: np.ndarray
@@ -34,3 +35,9 @@ class MomentSet:
     def decompose(self) -> np.ndarray:
         outer = np.array([self.mom[a] * self.mom[b] for a, b in _VOIGT_PAIRS])
         return self.stress - outer / self.rho
+
+
+try:   # the reference class itself when the reference package is on the path
+    from momentlbm.moments import MomentSet  # noqa: F401
+except ImportError:
+    MomentSet = _MomentSet

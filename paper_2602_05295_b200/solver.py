@@ -302,6 +302,28 @@ class Solver:
         self._last = StepStats._from_c(s)
         return self._last
 
+    def fluid_update(self, with_stats: bool = True):
+        """SPEC `fluid_update_step` (Alg. 2): the interior kernel over every
+        cell, no obstacle logic.  With obstacles the step is committed by ``solid_correction``."""
+        self.state_version += 1
+        self._chk(self._lib.hlbm_fluid_update(self._ctx, int(with_stats)))
+
+    def solid_correction(self) -> StepStats:
+        """SPEC `solid_correction_step`: the compacted boundary / solid / cut-link
+        kernels on the pending fluid update's output (identity when none is pending); returns the
+        step's StepStats (phase times t_fluid_ms / t_solid_ms)."""
+        self.state_version += 1
+        s = _lib.HlbmStats()
+        self._chk(self._lib.hlbm_solid_correction(self._ctx, C.byref(s)))
+        self._last = StepStats._from_c(s)
+        return self._last
+
+    def stream(self):
+        """The streaming operator S alone (no collision, not a time step): turns an Alg.-1
+        (post-collision) state into the split scheme's storage cut."""
+        self.state_version += 1
+        self._chk(self._lib.hlbm_stream(self._ctx))
+
     def step_percell(self, n: int = 1) -> StepStats:
         """Per-cell gather step with the same storage cut as ``step`` (one thread per cell pulls its
         sources, each re-evaluating the source's collision): the GPU cross-check of the split kernels."""
