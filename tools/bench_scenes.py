@@ -6,8 +6,9 @@ config 3: channel past a sphere 512x256x256 (inflow/outflow, periodic y/z), fp32
 config 4: procedural vehicle 1000x400x400, q16 + dither, inflow/outflow, periodic y/z
 Prints one JSON object per line: MLUPS (all cells), fluid-cell MLUPS, the split phase times
 (fluid_interior vs compacted boundary kernel), boundary-list sizes and, for voxel scenes, the
-time of the fused single-kernel Alg.-1 baseline -- the in-repo version of
-the paper's split / quantization attribution.
+time of the original HOME-LBM kernel (Alg. 1: own-population reconstruction into
+shared memory, 8^3 tiles, solid links inline, post-collision storage) -- the in-repo version of the
+paper's split / quantization attribution: fp32 Alg. 1 -> fp32 split -> q16 split.
 """
 import json
 import sys
@@ -89,6 +90,7 @@ def main():
     m = vehicle_mask(dims, seed=0)
     run("4 vehicle", dims, SolverConfig(nu=1e-5, bc=bc, u_in=(0.1, 0, 0), precision="q16",
                                         quant=QuantSpec(dither=True)), uniform(0.1), mask=m)
+    run("4 vehicle", dims, SolverConfig(nu=1e-5, bc=bc, u_in=(0.1, 0, 0), precision="fp32"), uniform(0.1), mask=m)
     mesh = voxel_surface_mesh(m)
     run("4b vehicle, triangle mesh", dims, SolverConfig(nu=1e-5, bc=bc, u_in=(0.1, 0, 0), precision="q16",
                                                         quant=QuantSpec(dither=True)), uniform(0.1), mesh=mesh)
