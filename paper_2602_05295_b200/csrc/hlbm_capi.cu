@@ -109,7 +109,8 @@ Geo make_geo(const hlbm_ctx* ctx, int xb = 0, int xr = -1) {
   const int nr = std::max(xr - xb, 0);
   g.xb = xb;
   g.xr = xr;
-  g.xseg = c.xseg > 0 ? std::min(c.xseg, std::max(nr, 1)) : auto_xseg(std::max(nr, 1), g.nzt * g.nyt, ctx->num_sms * kCtaPerSm);
+  g.xseg = c.xseg > 0 ? std::min(std::min(c.xseg, kMaxXseg), std::max(nr, 1))
+                      : auto_xseg(std::max(nr, 1), g.nzt * g.nyt, ctx->num_sms * kCtaPerSm);
   g.nxs = nr > 0 ? (nr + g.xseg - 1) / g.xseg : 0;
   g.gx0 = c.x0; g.gny = c.gny; g.gnz = c.gnz; g.gnx_total = c.gnx;
   return g;
@@ -198,7 +199,11 @@ int plane_offsets(hlbm_ctx* ctx, const int64_t* d_cells, int64_t n, std::vector<
   off.assign((size_t)c.nx + 1, n);
   if (n == 0) { std::fill(off.begin(), off.end(), 0); return HLBM_OK; }
   std::vector<int64_t> h((size_t)n);
-  CK(cudaMemcpy(h.data(), d_cells, n * 8, cudaMemcpyDeviceToHost));
+  // the list was built on the context's (non-blocking) stream: a legacy-stream cudaMemcpy would not
+  // wait for it (the offsets of the last list built by hlbm_set_mask / hlbm_set_mesh raced the
+  // compaction kernel and could misplace cells between the x-ranges of the overlapped step)
+  CK(cudaMemcpyAsync(h.data(), d_cells, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   int64_t i = 0;
   for (int x = 0; x <= c.nx; ++x) {
     while (i < n && h[(size_t)i] / pl < x) ++i;
@@ -812,6 +817,7 @@ int hlbm_get_cut_links(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, double* t
   if (!ctx || !n) return fail(ctx, HLBM_EINVAL, "null argument");
   const int64_t nb = ctx->mesh.nb;
   if (!cells) { *n = nb; return HLBM_OK; }
+  CK(cudaStreamSynchronize(ctx->stream));
   if (*n < nb) return fail(ctx, HLBM_EINVAL, "output buffer too small");
   *n = nb;
   if (nb == 0) return HLBM_OK;
@@ -830,6 +836,7 @@ int hlbm_get_boundary(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, int64_t* n
   if (*n < ctx->nb) return fail(ctx, HLBM_EINVAL, "output buffer too small");
   *n = ctx->nb;
   if (ctx->nb == 0) return HLBM_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaMemcpy(cells, ctx->d_bcells, ctx->nb * 8, cudaMemcpyDeviceToHost));
   if (masks) CK(cudaMemcpy(masks, ctx->d_bmasks, ctx->nb * 4, cudaMemcpyDeviceToHost));
   // local -> global linear index

@@ -459,21 +459,15 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     // mass, momentum, max |u|^2 -- accumulated before the encode (shorter live ranges of s and
     // 1/rho; measured 2.08 -> 2.02 ms for the STATS variant at 512^3) (NaN in any cell already makes the mass sum non-finite)
     const V ju = vmul(vfma(s[3], s[3], vfma(s[2], s[2], vmul(s[1], s[1]))), vmul(inv, inv));
-    if (statx && staty) {
-      const V a = vadd(make_float2(s[0].x, s[1].x), make_float2(s[0].y, s[1].y));
-      const V c = vadd(make_float2(s[2].x, s[3].x), make_float2(s[2].y, s[3].y));
-      acc[0] += a.x; acc[32] += a.y; acc[64] += c.x; acc[96] += c.y;
-      acc[128] = fmaxf(acc[128], fmaxf(ju.x, ju.y));
-    } else {
-      if (statx) {
-        acc[0] += s[0].x; acc[32] += s[1].x; acc[64] += s[2].x; acc[96] += s[3].x;
-        acc[128] = fmaxf(acc[128], ju.x);
-      }
-      if (staty) {
-        acc[0] += s[0].y; acc[32] += s[1].y; acc[64] += s[2].y; acc[96] += s[3].y;
-        acc[128] = fmaxf(acc[128], ju.y);
-      }
-    }
+    // branch-free: excluded (boundary / solid) cells contribute zeros through selects, so a warp
+    // holding special cells does not diverge (the divergent form cost ~15% of the STATS step of
+    // a 512x256x256 scene with a mesh)
+    const V a = vadd(make_float2(statx ? s[0].x : 0.f, statx ? s[1].x : 0.f),
+                     make_float2(staty ? s[0].y : 0.f, staty ? s[1].y : 0.f));
+    const V c = vadd(make_float2(statx ? s[2].x : 0.f, statx ? s[3].x : 0.f),
+                     make_float2(staty ? s[2].y : 0.f, staty ? s[3].y : 0.f));
+    acc[0] += a.x; acc[32] += a.y; acc[64] += c.x; acc[96] += c.y;
+    acc[128] = fmaxf(acc[128], fmaxf(statx ? ju.x : 0.f, staty ? ju.y : 0.f));
   }
   const int64_t plane_off = (int64_t)(q + 1) * g.pstride;
   const int64_t cell_off = plane_off + cell_off0;
@@ -605,6 +599,33 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&A.tmap_in)) : "memory");
   }
+  // STATS + SPECIAL: the special-cell bits of the CTA's whole tile (planes xs..xe-1, its kRows rows,
+  // the 64-cell window of each row as two words: bit 2l / 2l+1 = lane l's cells) are copied to
+  // shared memory once, before the march.  A global load per plane instead left its DRAM latency
+  // on a scoreboard the plane's loop waited on (+16% on the STATS step of a scene with solids).
+  uint32_t (*sbm)[2] = reinterpret_cast<uint32_t (*)[2]>(smem_raw + sizeof(Sm));
+  if (STATS && SPECIAL) {
+    const int z0 = zs0 - kZOff;                 // logical z of bit 0 of the window
+    const int wa = z0 >= 0 ? (z0 >> 5) : -1;    // first bitmask word touched
+    const int sh = z0 - 32 * wa;                // 0..31
+    for (int i = threadIdx.x; i < (xe - xs) * kRows; i += blockDim.x) {
+      const int pl = xs + i / kRows, r = y0 + i % kRows;
+      uint32_t lo = 0, hi = 0;
+      if (r < g.ny) {
+        const uint32_t* row = A.special_bits + ((int64_t)pl * g.ny + r) * A.bits_row_words;
+        uint32_t wv[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int idx = wa + k;   // bits beyond nz are zero in the bitmask
+          wv[k] = (idx >= 0 && idx < A.bits_row_words) ? __ldg(row + idx) : 0u;
+        }
+        lo = __funnelshift_r(wv[0], wv[1], sh);
+        hi = __funnelshift_r(wv[1], wv[2], sh);
+      }
+      sbm[i][0] = lo;
+      sbm[i][1] = hi;
+    }
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int it = 0; it < STAGES && it < NP; ++it)
@@ -669,6 +690,11 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
       const int p = xs - 1 + it;
       const int q = p - 1;   // destination plane finished in this iteration
       const bool store_plane = wr && it >= 2;
+      // STATS + SPECIAL: boundary / solid cells are finished by the compacted kernels and stay out
+      // of the statistics; their two bits come from the CTA's shared-memory copy of the bitmask
+      uint32_t sbits = 0;
+      if (STATS && SPECIAL && store_plane)
+        sbits = (sbm[(q - xs) * kRows + (w - 1)][lane >> 4] >> (2 * (lane & 15))) & 3u;
       const int b = (NB == 2) ? (it & 1) : 0;
       const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
       V (*exch)[kNW][32] = S.exch[b];
@@ -695,13 +721,7 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
       mbar_arrive(&S.empty[b][wu]);
       mbar_arrive(&S.empty[b][wd]);
       if (store_plane) {
-        bool sx = STATS, sy = STATS;
-        if (STATS && SPECIAL) {   // boundary / solid cells are finished by the compacted kernels
-          const uint32_t wv =
-              __ldg(A.special_bits + ((int64_t)q * g.ny + yrow) * A.bits_row_words + (zc >> 5));
-          sx = !((wv >> (zc & 31)) & 1u);
-          sy = !((wv >> ((zc & 31) + 1)) & 1u);
-        }
+        const bool sx = STATS && !(sbits & 1u), sy = STATS && !(sbits & 2u);
         store_pair<Q16, DITHER, STATS, QMODE>(A, fin, q, yrow, zc, cell0, sx, sy, acc);
       }
     };
@@ -776,7 +796,9 @@ template <bool Q16, bool FORCE, bool SPECIAL, bool DITHER, bool STATS, int QMODE
 static cudaError_t launch_interior_t(const StepArgs& A, int nblocks, cudaStream_t st) {
   constexpr int STAGES = InteriorCfg<Q16, LAT>::STAGES, NB = InteriorCfg<Q16, LAT>::NB;
   constexpr int NC = Q16 ? 5 : 10;
-  const size_t smem = sizeof(Smem<NC, STAGES, NB, LatSlots<LAT>::n>);
+  // STATS + SPECIAL: + the tile's special-cell bitmask (kMaxXseg planes x kRows rows x 64 bits)
+  const size_t smem = sizeof(Smem<NC, STAGES, NB, LatSlots<LAT>::n>) +
+                      ((STATS && SPECIAL) ? (size_t)kMaxXseg * kRows * 8 : 0);
   auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STATS, QMODE, STAGES, NB, LAT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -32,6 +32,7 @@ constexpr int kZW = 64;          // z cells covered by one warp (32 lanes x 2 ce
 constexpr int kZT = 60;          // interior z cells per tile (lanes 1..30; lanes 0 and 31 are halo)
 constexpr int kZOff = 2;         // storage column of z = 0
 constexpr int kNSlot = 18;       // exchanged values per cell pair: (cx 3) x (cy +-1) x (kz 3)
+constexpr int kMaxXseg = 128;    // longest x segment of one interior CTA (auto_xseg caps here too)
 
 struct Geo {
   int nx, ny, nz;          // local interior dims (x = slab axis)

@@ -1,7 +1,7 @@
 """SPEC.md:497 property, measured: the fluid-update phase time is independent of the triangle
 count (within +-10% from 0 to ~10^5 triangles at a fixed grid), and the solid-correction time grows
-at most linearly in the cut-link work.  The same sphere (radius 20 in a 256 x 128 x 128 channel,
-16-bit state) is tessellated with 0 .. 81920 triangles; each StepStats carries the device times of
+at most linearly in the cut-link work.  The paper's sphere scene size (512 x 256 x 256, PAPER.md
+Table 1; a radius-32 sphere, 16-bit state) is tessellated with 0 .. 81920 triangles; each StepStats carries the device times of
 the fluid update (interior kernel) and of the solid correction (compacted cut-link kernel)."""
 
 import numpy as np
@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 
 def test_fluid_update_time_independent_of_triangle_count():
-    dims = (256, 128, 128)
+    dims = (512, 256, 256)
     cfg = SolverConfig(nu=1e-3, precision="q16", bc={"x": ("inflow", "outflow"), "y": ("periodic", "periodic"),
                                                       "z": ("periodic", "periodic")}, u_in=(0.05, 0, 0))
     rows = []
@@ -22,7 +22,7 @@ def test_fluid_update_time_independent_of_triangle_count():
         with Solver(SimGrid(dims), cfg) as s:
             ntri = 0
             if subdiv is not None:
-                V, F = M.icosphere((96.3, 63.7, 64.1), 20.0, subdiv)
+                V, F = M.icosphere((128.3, 127.7, 128.1), 32.0, subdiv)
                 s.set_mesh(V, F)
                 ntri = len(F)
             s.init_modes(np.array([[0, 0, 0, 0.05, 0, 0, np.pi / 2]]))
