@@ -171,3 +171,60 @@ def voxel_surface_mesh(mask):
     if not verts:
         return np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int32)
     return np.concatenate(verts), np.concatenate(faces).astype(np.int32)
+
+
+def load_obj(path, transform=None):
+    """Wavefront OBJ -> (vertices (nv, 3) float64, faces (nf, 3) int32); SPEC.md:404-407 `load_mesh`.
+
+    Reads `v` and `f` records only (`vt` / `vn` / `o` / `g` / `s` / comments are skipped); face
+    entries may be `i`, `i/t`, `i//n` or `i/t/n`, 1-based or negative (relative); polygons are fan-
+    triangulated.  ``transform`` is a 3x4 (or 4x4) affine matrix applied to the vertices (lattice
+    coordinates).  Malformed records raise ValueError naming the line; degenerate faces (repeated
+    vertices or zero area) raise ValueError naming the face index."""
+    verts, faces = [], []
+    with open(path, "r") as f:
+        for ln, line in enumerate(f, 1):
+            s = line.split("#", 1)[0].strip()
+            if not s:
+                continue
+            tok = s.split()
+            if tok[0] == "v":
+                if len(tok) < 4:
+                    raise ValueError(f"{path}:{ln}: vertex record needs 3 coordinates")
+                try:
+                    verts.append([float(t) for t in tok[1:4]])
+                except ValueError:
+                    raise ValueError(f"{path}:{ln}: malformed vertex record") from None
+            elif tok[0] == "f":
+                if len(tok) < 4:
+                    raise ValueError(f"{path}:{ln}: face record needs at least 3 vertices")
+                idx = []
+                for t in tok[1:]:
+                    try:
+                        i = int(t.split("/")[0])
+                    except ValueError:
+                        raise ValueError(f"{path}:{ln}: malformed face entry {t!r}") from None
+                    i = i - 1 if i > 0 else len(verts) + i
+                    if i < 0 or i >= len(verts) or int(t.split("/")[0]) == 0:
+                        raise ValueError(f"{path}:{ln}: face index {t!r} out of range")
+                    idx.append(i)
+                for k in range(1, len(idx) - 1):
+                    faces.append((idx[0], idx[k], idx[k + 1]))
+    V = np.array(verts, dtype=np.float64).reshape(-1, 3)
+    F = np.array(faces, dtype=np.int32).reshape(-1, 3)
+    if transform is not None:
+        T = np.asarray(transform, dtype=np.float64)
+        V = V @ T[:3, :3].T + T[:3, 3]
+    for fi, (a, b, c) in enumerate(F):
+        if a == b or b == c or a == c or np.linalg.norm(np.cross(V[b] - V[a], V[c] - V[a])) == 0.0:
+            raise ValueError(f"{path}: degenerate face {fi} (vertices {a}, {b}, {c})")
+    return V, F
+
+
+def save_obj(path, vertices, faces):
+    """Write (vertices, faces) as a Wavefront OBJ (1-based `v` / `f` records)."""
+    with open(path, "w") as f:
+        for v in np.asarray(vertices, dtype=np.float64):
+            f.write(f"v {float(v[0])!r} {float(v[1])!r} {float(v[2])!r}\n")
+        for a, b, c in np.asarray(faces, dtype=np.int64):
+            f.write(f"f {a + 1} {b + 1} {c + 1}\n")

@@ -27,6 +27,7 @@ streaming operator S once, (S o C)^n o S = S o (C o S)^n.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -37,6 +38,7 @@ from momentlbm.moments import MomentSet
 
 from paper_2602_05295_b200 import QuantSpec
 from paper_2602_05295_b200 import io as _io
+from paper_2602_05295_b200.geometry import load_obj
 from paper_2602_05295_b200 import solver as _b200
 from paper_2602_05295_b200.solver import StepStats
 
@@ -63,8 +65,8 @@ def _face_spec(spec):
 class SolverConfig:
     """lattice kind, nu (tau = 0.5 + 3 nu, collision.py:30-31), body force F,
     boundary condition per face (periodic | inflow(velocity) | outflow | wall), quantization preset
-    ("16/16" ... "12/11", a QuantSpec) or None, obstacle list (voxel masks and/or triangle meshes
-    (vertices, faces) in lattice coordinates).  ``dims`` / ``initial`` let ``run(config, steps)``
+    ("16/16" ... "12/11", a QuantSpec) or None, obstacle list (voxel masks, triangle meshes
+    (vertices, faces[, motion]) in lattice coordinates, or Wavefront OBJ paths).  ``dims`` / ``initial`` let ``run(config, steps)``
     build its own grid (``initial``: None = rest, or a (rho, mom, stress) triple)."""
     lattice: str = "D3Q27"
     nu: float = 0.01
@@ -149,6 +151,8 @@ class SimGrid:
         mask = self.mask
         meshes = []
         for ob in config.obstacles:
+            if isinstance(ob, (str, os.PathLike)):      # Wavefront OBJ (SPEC.md:404-407 load_mesh)
+                ob = load_obj(ob)
             if isinstance(ob, np.ndarray):
                 m = np.asarray(ob, dtype=np.uint8)
                 mask = m if mask is None else (mask | m)
@@ -161,7 +165,8 @@ class SimGrid:
         s = _b200.Solver(_b200.SimGrid(self.dims, mask), cfg)
         if meshes:
             V, F = meshes[0][:2]
-            s.set_mesh(V, F)
+            motion = meshes[0][2] if len(meshes[0]) > 2 else {}
+            s.set_mesh(V, F, **motion)     # motion: {velocity, omega, center} (SPEC SolidState)
         init = carried if carried is not None else self._pending
         if init is not None:
             s.set_moments(*init)

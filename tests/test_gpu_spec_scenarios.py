@@ -1,0 +1,133 @@
+"""SPEC integration properties on the GPU path:
+
+  * Taylor vortex (z-invariant 2-D flow on a 64 x 64 x 4 periodic slab, nu = 0.01): the velocity
+    amplitude decays as exp(-2 nu k^2 t) within 2% for the split step (fp32 and q16) and for the
+    original HOME-LBM kernel (Alg. 1);
+  * double-layer vortex at 256^2, 16-bit moments: stays finite with rho saturation events < 0.1% of
+    the samples (cells x steps), and the Fig.-11 sweep at 256^2: l2 velocity error non-decreasing as
+    bits decrease (10% noise band), 16/16 bytes/node exactly 50% of fp32;
+  * periodic fluid-only run: total mass and momentum conserved;
+  * a triangle mesh loaded from a Wavefront OBJ file drives the same cut-link table as the arrays.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import mesh as M
+from oracle.moments import neq_recompose
+from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
+from paper_2602_05295_b200.geometry import load_obj, save_obj
+from paper_2602_05295_b200.sweep import DEFAULT_PRESETS, Scenario, quant_sweep
+
+pytestmark = pytest.mark.gpu
+
+
+def _taylor(n, u0):
+    k = 2 * np.pi / n
+    x = np.arange(n)[:, None, None]
+    y = np.arange(n)[None, :, None]
+    ux = u0 * np.sin(k * x) * np.cos(k * y) * np.ones((1, 1, 4))
+    uy = -u0 * np.cos(k * x) * np.sin(k * y) * np.ones((1, 1, 4))
+    rho = 1.0 - 3.0 * (u0 ** 2 / 4.0) * (np.cos(2 * k * x) + np.cos(2 * k * y)) * np.ones((1, 1, 4))
+    u = np.stack([ux, uy, np.zeros_like(ux)])
+    mom = rho * u
+    return rho, mom, neq_recompose(rho, mom, np.zeros((6,) + rho.shape)), k
+
+
+@pytest.mark.parametrize("scheme", ["split_fp32", "split_q16_dither", "alg1_fp32"])
+def test_taylor_vortex_analytic_decay(scheme):
+    n, u0, nu = 64, 0.02, 0.01
+    rho, mom, st, k = _taylor(n, u0)
+    shape_x = np.sin(k * np.arange(n))[:, None, None] * np.cos(k * np.arange(n))[None, :, None]
+    cfg = SolverConfig(nu=nu, precision="q16" if "q16" in scheme else "fp32",
+                       quant=QuantSpec(dither="dither" in scheme))
+    amps = []
+    with Solver(SimGrid((n, n, 4)), cfg) as s:
+        s.set_moments(rho, mom, st)
+        for _ in range(4):
+            if scheme.startswith("alg1"):
+                s.step_fused(500)
+            else:
+                s.step(500)
+            ux = s.velocity[0]
+            amps.append(float((ux * shape_x).sum() / (shape_x ** 2 * np.ones((1, 1, 4))).sum()))
+    t = 500 * np.arange(1, 5)
+    ana = u0 * np.exp(-2 * nu * k * k * t)
+    rel = np.abs(np.array(amps) / ana - 1)
+    print(scheme, "amplitude / analytic - 1 at t = 500..2000:", rel)
+    assert rel.max() < 0.02
+
+
+def test_taylor_vortex_dither_removes_the_rounding_bias():
+    """Without dither the 16-bit rounding is deterministic and biases the decay (4% at t = 2000,
+    amplitude 0.013 = 700 LSB of rho u); the counter-hash dither makes it unbiased."""
+    n, u0, nu = 64, 0.02, 0.01
+    rho, mom, st, k = _taylor(n, u0)
+    shape_x = np.sin(k * np.arange(n))[:, None, None] * np.cos(k * np.arange(n))[None, :, None]
+    out = {}
+    for dither in (False, True):
+        with Solver(SimGrid((n, n, 4)), SolverConfig(nu=nu, precision="q16", quant=QuantSpec(dither=dither))) as s:
+            s.set_moments(rho, mom, st)
+            s.step(2000)
+            ux = s.velocity[0]
+        amp = float((ux * shape_x).sum() / (shape_x ** 2 * np.ones((1, 1, 4))).sum())
+        out[dither] = abs(amp / (u0 * np.exp(-2 * nu * k * k * 2000)) - 1)
+    print("t = 2000, |amplitude / analytic - 1|: no dither", out[False], "dither", out[True])
+    assert out[True] < 0.005 and out[False] > 5 * out[True]
+
+
+def test_double_layer_vortex_q16_finite_low_saturation():
+    sc = Scenario(n=256, steps=2000)
+    rho, u = sc.initial()
+    cfg = SolverConfig(nu=sc.nu, precision="q16", quant=QuantSpec())
+    sat = 0
+    with Solver(SimGrid((sc.n, sc.n, sc.nz)), cfg) as s:
+        s.set_equilibrium(rho, u)
+        for _ in range(sc.steps // 10):
+            st = s.step(10)                    # raises FloatingPointError on divergence
+            sat += int(st.saturation[0]) * 10  # rho saturations of the sampled step, x its batch
+        vel = s.velocity
+    samples = sc.n * sc.n * sc.nz * sc.steps
+    print(f"double-layer 256^2 x {sc.steps}: rho saturation ~{sat} of {samples} samples, max|u| {np.abs(vel).max():.3f}")
+    assert np.all(np.isfinite(vel))
+    assert sat < 1e-3 * samples
+
+
+def test_quant_sweep_256_monotone():
+    """With dither the l2 error grows monotonically as bits drop.  Without it the
+    deterministic rounding bias dominates and 16/16 comes out above 16/15."""
+    sc = Scenario(n=256, steps=1000)
+    rows = quant_sweep(sc, dither=True)
+    err = {r["config"]: r["l2_rel_error"] for r in rows}
+    e = [err[p] for p in DEFAULT_PRESETS]
+    print("sweep 256^2:", {p: f"{v:.2e}" for p, v in zip(DEFAULT_PRESETS, e)})
+    assert all(b >= a * 0.9 for a, b in zip(e, e[1:]))
+    assert e[-1] > e[0]
+    by = {r["config"]: r["bytes_stored"] for r in rows}
+    assert by["16/16"] * 2 == by["fp32"]
+
+
+def test_periodic_mass_momentum_conservation_1000_steps():
+    from oracle import step as OS
+    shape = (32, 32, 32)
+    state = OS.random_state(shape, seed=3, drho=0.02, umax=0.03, sneq=0.002)
+    with Solver(SimGrid(shape), SolverConfig(nu=0.02)) as s:
+        s.set_moments(*state)
+        m0 = s.step(1)
+        m1 = s.step(999)
+    assert abs(m1.mass - m0.mass) / m0.mass < 1e-7          # fp32 state (SPEC's 1e-10 is for 64-bit)
+    np.testing.assert_allclose(m1.momentum, m0.momentum, atol=1e-6 * np.prod(shape) * 0.03)
+
+
+def test_obj_mesh_drives_the_same_cut_links(tmp_path):
+    V, F = M.icosphere((11.3, 9.7, 13.9), 5.2, 2)
+    p = tmp_path / "sphere.obj"
+    save_obj(p, V, F)
+    V2, F2 = load_obj(p)
+    res = []
+    for VV, FF in ((V, F), (V2, F2)):
+        with Solver(SimGrid((24, 20, 28)), SolverConfig(nu=0.02)) as s:
+            s.set_mesh(VV, FF)
+            res.append(s.cut_links())
+    for a, b in zip(res[0], res[1]):
+        assert np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
