@@ -54,6 +54,8 @@ struct hlbm_ctx {
   std::vector<int64_t> off_b, off_s, off_m;   // per-plane offsets (nx+1) into the sorted lists
   int pending_stats = 0;                      // statistics requested for the step in progress
   int pending_solid = 0;                      // hlbm_fluid_update ran, its solid correction not yet
+  double* d_stage = nullptr;                  // host<->device staging of the float64 import/export
+  size_t stage_bytes = 0;
   int64_t steps = 0;
   int64_t launches = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -92,6 +94,18 @@ int auto_xseg(int nx, int tiles_yz, int sms) {
     }
   }
   return best;
+}
+
+// device staging buffer of at least `bytes` (kept for later calls)
+int staging(hlbm_ctx* ctx, size_t bytes) {
+  if (ctx->stage_bytes >= bytes) return HLBM_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(ctx->d_stage);
+  ctx->d_stage = nullptr;
+  ctx->stage_bytes = 0;
+  CK(cudaMalloc(&ctx->d_stage, bytes));
+  ctx->stage_bytes = bytes;
+  return HLBM_OK;
 }
 
 Geo make_geo(const hlbm_ctx* ctx, int xb = 0, int xr = -1) {
@@ -471,6 +485,7 @@ void hlbm_destroy(hlbm_ctx* ctx) {
   cudaFree(ctx->d_scells);
   cudaFree(ctx->d_bits);
   cudaFree(ctx->d_fused);
+  cudaFree(ctx->d_stage);
   free_mesh(ctx);
   for (int i = 0; i < 3; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -530,15 +545,17 @@ int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const 
   SETTLE(ctx);
   const hlbm_config& c = ctx->cfg;
   const int64_t n = (int64_t)c.nx * c.ny * c.nz;
-  for (int64_t i = 0; i < n; ++i)
-    if (!(rho[i] > 0.0)) return fail(ctx, HLBM_EINVAL, "density must be positive");   // moments.py:147
   const int64_t pl = (int64_t)c.ny * c.nz;
   const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(c.nx, (64ll << 20) / (pl * 80)));
-  double *dr, *dm, *ds;
-  CK(cudaMalloc(&dr, chunk * pl * 8));
-  CK(cudaMalloc(&dm, 3 * chunk * pl * 8));
-  CK(cudaMalloc(&ds, 6 * chunk * pl * 8));
+  if (int r = staging(ctx, (size_t)chunk * pl * 10 * 8)) return r;   // reused across calls
+  double* dr = ctx->d_stage;
+  double* dm = dr + (size_t)chunk * pl;
+  double* ds = dm + (size_t)3 * chunk * pl;
+  // import into the spare buffer; it becomes current only if every density is positive
+  // (moments.py:147), so a rejected call leaves the state untouched.  The check runs on the device.
+  void* spare = ctx->buf[1 - ctx->cur];
   CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
+  unsigned int* nonpos = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ctx->d_stats) + offsetof(Stats, nonfinite));
   const Geo g = make_geo(ctx);
   for (int x0 = 0; x0 < c.nx; x0 += chunk) {
     const int cnt = std::min(chunk, c.nx - x0);
@@ -548,15 +565,15 @@ int hlbm_set_moments(hlbm_ctx* ctx, const double* rho, const double* mom, const 
       CK(cudaMemcpyAsync(dm + k * m, mom + k * n + x0 * pl, m * 8, cudaMemcpyHostToDevice, ctx->stream));
     for (int k = 0; k < 6; ++k)
       CK(cudaMemcpyAsync(ds + k * m, stress + k * n + x0 * pl, m * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CK(launch_import(g, ctx->RG, ctx->q16, ctx->buf[ctx->cur], dr, dm, ds, x0, cnt,
-                     sat_ptr(ctx), ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(launch_import(g, ctx->RG, ctx->q16, spare, dr, dm, ds, x0, cnt, sat_ptr(ctx), nonpos, ctx->stream));
   }
-  CK(launch_fill_ghosts(g, ctx->NC, ctx->buf[ctx->cur], ctx->stream));
+  unsigned int bad = 0;
+  CK(cudaMemcpyAsync(&bad, nonpos, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(dr);
-  cudaFree(dm);
-  cudaFree(ds);
+  if (bad) return fail(ctx, HLBM_EINVAL, "density must be positive");
+  CK(launch_fill_ghosts(g, ctx->NC, spare, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->cur = 1 - ctx->cur;
   return HLBM_OK;
 }
 
@@ -570,10 +587,10 @@ int hlbm_get_moments_box(hlbm_ctx* ctx, int32_t x0, int32_t cx, int32_t y0, int3
   if (pl == 0 || cx == 0) return HLBM_OK;
   const int64_t n = pl * cx;
   const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(cx, (64ll << 20) / (pl * 80)));
-  double *dr, *dm, *ds;
-  CK(cudaMalloc(&dr, chunk * pl * 8));
-  CK(cudaMalloc(&dm, 3 * chunk * pl * 8));
-  CK(cudaMalloc(&ds, 6 * chunk * pl * 8));
+  if (int r = staging(ctx, (size_t)chunk * pl * 10 * 8)) return r;
+  double* dr = ctx->d_stage;
+  double* dm = dr + (size_t)chunk * pl;
+  double* ds = dm + (size_t)3 * chunk * pl;
   const Geo g = make_geo(ctx);
   for (int xa = 0; xa < cx; xa += chunk) {
     const int cnt = std::min(chunk, cx - xa);
@@ -587,9 +604,6 @@ int hlbm_get_moments_box(hlbm_ctx* ctx, int32_t x0, int32_t cx, int32_t y0, int3
       CK(cudaMemcpyAsync(stress + k * n + xa * pl, ds + k * m, m * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
-  cudaFree(dr);
-  cudaFree(dm);
-  cudaFree(ds);
   return HLBM_OK;
 }
 

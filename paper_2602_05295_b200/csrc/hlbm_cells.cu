@@ -10,6 +10,7 @@
 //   classify / compact   voxel mask -> sorted boundary-cell list + 27-bit link masks and the
 //                   solid list, deterministic (block prefix sums, no atomics in the ordering).
 //   import / export reference layout (rho, mom, stress float64) <-> internal state.
+#include <algorithm>
 #include <climits>
 
 #include "hlbm_launch.h"
@@ -422,10 +423,95 @@ cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool
   return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------------------------ compacted lists, three warps per 32 cells
+// The voxel boundary-cell list of the split scheme (MODE 0: half-way bounce-back) runs in
+// blocks of 3 warps over 32 consecutive list entries: warp w takes the links with c_x = w - 1 (9 of
+// the 27), lane l the l-th cell, so each link's loads stay coalesced across the lanes (consecutive
+// boundary cells are mostly consecutive in z) while three times as many independent link chains are
+// in flight as with one thread walking all 27 links.  The three partial raw-moment sums meet in
+// shared memory and are added in a fixed order (deterministic); warp 0 finishes the cell.
+template <int I, int CXW, bool Q16, bool FORCE, int MODE, int Q>
+struct PullGroup {
+  __device__ __forceinline__ static void run(const StepArgs& A, int x, int y, int z, uint32_t mask, float m[10],
+                                             MeshCtx& mc) {
+    if constexpr (kCX[I] == CXW) pull_link<I, Q16, FORCE, MODE, Q>(A, x, y, z, mask, m, mc);
+    PullGroup<I + 1, CXW, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
+  }
+};
+template <int CXW, bool Q16, bool FORCE, int MODE, int Q>
+struct PullGroup<Q, CXW, Q16, FORCE, MODE, Q> {
+  __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*, MeshCtx&) {}
+};
+
+template <bool Q16, bool FORCE, bool DITHER, int MODE, int Q>
+__global__ void __launch_bounds__(96) pull_list3(const __grid_constant__ StepArgs A,
+                                                 const int64_t* __restrict__ cells,
+                                                 const uint32_t* __restrict__ masks, int64_t n) {
+  __shared__ float part[2][10][32];   // the c_x = 0 and +1 warps' partial sums
+  const Geo& g = A.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float red[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  MeshCtx mc;   // unused by MODE 0
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < n; base += (int64_t)gridDim.x * 32) {
+    const int64_t idx = base + lane;
+    const bool valid = idx < n;
+    float m[10];
+#pragma unroll
+    for (int c = 0; c < 10; ++c) m[c] = 0.f;
+    int x = 0, y = 0, z = 0;
+    if (valid) {
+      const int64_t cell = cells[idx];
+      const int64_t yz = (int64_t)g.ny * g.nz;
+      x = (int)(cell / yz);
+      const int64_t r = cell - (int64_t)x * yz;
+      y = (int)(r / g.nz);
+      z = (int)(r - (int64_t)y * g.nz);
+      const uint32_t mask = masks[idx];
+      if (w == 0) PullGroup<0, -1, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
+      else if (w == 1) PullGroup<0, 0, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
+      else PullGroup<0, 1, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
+    }
+    if (w > 0) {
+#pragma unroll
+      for (int c = 0; c < 10; ++c) part[w - 1][c][lane] = m[c];
+    }
+    __syncthreads();
+    if (w == 0 && valid) {
+#pragma unroll
+      for (int c = 0; c < 10; ++c) m[c] = (m[c] + part[0][c][lane]) + part[1][c][lane];
+      float st[10];
+      raw_to_state<float>(m, st);
+      store_cell<Q16, DITHER>(A, x, y, z, st, A.do_stats != 0, red);
+    }
+    __syncthreads();
+  }
+  if (A.do_stats && w == 0) flush_stats(A, red);
+}
+
 cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uint32_t* masks,
                               int64_t n, int mode, bool q16, bool force, bool dither,
                               cudaStream_t st, int q, int64_t base) {
   if (n <= 0) return cudaSuccess;
+  // voxel boundary lists: 3 warps per 32 cells (the mesh lists keep one thread per cell: their
+  // Eq.-8 context -- the cell's own collision -- would be recomputed by each of the three warps;
+  // measured 2.86 vs 2.77 ms on the 505k-triangle vehicle)
+  if (cells && mode == 0 && base == 0) {
+    const int64_t nblk = std::min<int64_t>((n + 31) / 32, (int64_t)148 * 16);
+#define HLBM_PL3(QQ, F, D)                                                                                  \
+    if (q16 == QQ && force == F && dither == D) {                                                           \
+      if (q == 19) pull_list3<QQ, F, D, 0, 19><<<(unsigned)nblk, 96, 0, st>>>(A, cells, masks, n);            \
+      else pull_list3<QQ, F, D, 0, 27><<<(unsigned)nblk, 96, 0, st>>>(A, cells, masks, n);                     \
+      return cudaGetLastError();                                                                            \
+    }
+    HLBM_PL3(false, false, false)
+    HLBM_PL3(false, true, false)
+    HLBM_PL3(true, false, false)
+    HLBM_PL3(true, true, false)
+    HLBM_PL3(true, false, true)
+    HLBM_PL3(true, true, true)
+#undef HLBM_PL3
+    return cudaErrorInvalidValue;
+  }
   const int tpb = 128;
   const int64_t nb = (n + tpb - 1) / tpb;
 #define HLBM_PULL(QQ, F, D)                                                                                    \
@@ -606,13 +692,14 @@ __global__ void special_bits_kernel(const uint8_t* __restrict__ cls, int nx, int
 template <bool Q16>
 __global__ void import_f64(Geo g, Ranges R, void* dst, const double* __restrict__ rho,
                            const double* __restrict__ mom, const double* __restrict__ stress, int x0,
-                           int cnt, unsigned long long* __restrict__ sat) {
+                           int cnt, unsigned long long* __restrict__ sat, unsigned int* __restrict__ nonpos) {
   const int64_t yz = (int64_t)g.ny * g.nz, n = yz * cnt;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int xl = (int)(i / yz);
     const int64_t r = i - (int64_t)xl * yz;
     const double rh = rho[i];
+    if (!(rh > 0.0)) atomicAdd(nonpos, 1u);   // moments.py:147 "density must be positive" (host rejects)
     const double j0 = mom[i], j1 = mom[n + i], j2 = mom[2 * n + i];
     // sneq = stress - mom mom / rho  (moments.py:93-96, _outer_voigt :124-133)
     const double v[10] = {rh,
@@ -779,8 +866,8 @@ __global__ void pack_codes(Geo g, int NC, const uint32_t* __restrict__ buf, uint
   }
 }
 
-template __global__ void import_f64<false>(Geo, Ranges, void*, const double*, const double*, const double*, int, int, unsigned long long*);
-template __global__ void import_f64<true>(Geo, Ranges, void*, const double*, const double*, const double*, int, int, unsigned long long*);
+template __global__ void import_f64<false>(Geo, Ranges, void*, const double*, const double*, const double*, int, int, unsigned long long*, unsigned int*);
+template __global__ void import_f64<true>(Geo, Ranges, void*, const double*, const double*, const double*, int, int, unsigned long long*, unsigned int*);
 
 }  // namespace hlbm
 
@@ -795,10 +882,10 @@ static unsigned grid_for(int64_t n, int tpb) {
 
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
                           const double* mom, const double* stress, int x0, int cnt,
-                          unsigned long long* sat, cudaStream_t st) {
+                          unsigned long long* sat, unsigned int* nonpos, cudaStream_t st) {
   const int64_t n = (int64_t)g.ny * g.nz * cnt;
-  if (q16) import_f64<true><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho, mom, stress, x0, cnt, sat);
-  else import_f64<false><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho, mom, stress, x0, cnt, sat);
+  if (q16) import_f64<true><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho, mom, stress, x0, cnt, sat, nonpos);
+  else import_f64<false><<<grid_for(n, 256), 256, 0, st>>>(g, R, dst, rho, mom, stress, x0, cnt, sat, nonpos);
   return cudaGetLastError();
 }
 

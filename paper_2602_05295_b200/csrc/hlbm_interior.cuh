@@ -800,8 +800,12 @@ static cudaError_t launch_interior_t(const StepArgs& A, int nblocks, cudaStream_
   const size_t smem = sizeof(Smem<NC, STAGES, NB, LatSlots<LAT>::n>) +
                       ((STATS && SPECIAL) ? (size_t)kMaxXseg * kRows * 8 : 0);
   auto k = fluid_interior<Q16, FORCE, SPECIAL, DITHER, STATS, QMODE, STAGES, NB, LAT>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static bool attr = false;   // once per instantiation, not on every launch
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   k<<<nblocks, kNW * 32, smem, st>>>(A);
   return cudaGetLastError();
 }

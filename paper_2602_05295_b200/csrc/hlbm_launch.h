@@ -47,7 +47,7 @@ cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool
                         cudaStream_t st, bool collide);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
                           const double* mom, const double* stress, int x0, int cnt,
-                          unsigned long long* sat, cudaStream_t st);
+                          unsigned long long* sat, unsigned int* nonpos, cudaStream_t st);
 cudaError_t launch_export(const Geo& g, const Ranges& R, bool q16, const void* src, double* rho,
                           double* mom, double* stress, int x0, int cx, int y0, int cy, int z0, int cz,
                           cudaStream_t st);
