@@ -248,7 +248,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   StepArgs A = make_args(ctx, with_stats, xb, xr);
-  const bool fast19 = ctx->q == 19 && (!q16 || ctx->qmode == 2);
+  const bool fast19 = ctx->q == 19;   // every D3Q19 codec runs the two-chain interior kernel
   if (ctx->q == 19 && !fast19) {
     // D3Q19 with a non-default codec: the per-cell fused kernel over the planes of the range,
     // solid links inline (no separate correction phase)
@@ -262,7 +262,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   }
   if (phases & kPhaseFluid) {
     if (fast19)   // D3Q19: two-chain streaming; solids through the compacted 19-link kernels below
-      CK(launch_fluid_interior19(A, q16, force, special, dither, st));
+      CK(launch_fluid_interior19(A, q16, force, special, dither, ctx->qmode, st));
     else
       CK(launch_fluid_interior(A, q16, force, special, dither, ctx->qmode, st));
     ++ctx->launches;
@@ -866,7 +866,7 @@ int hlbm_fluid_update(hlbm_ctx* ctx, int32_t with_stats) {
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (int r = run_range(ctx, 0, ctx->cfg.nx, with_stats, ctx->ev[1], nullptr, kPhaseFluid)) return r;
   ctx->pending_stats = with_stats ? 1 : 0;
-  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0 && !(ctx->q == 19 && ctx->q16 && ctx->qmode != 2);
+  const bool special = ctx->nb + ctx->ns + ctx->mesh.nb > 0;
   if (special) {
     ctx->pending_solid = 1;
     return HLBM_OK;

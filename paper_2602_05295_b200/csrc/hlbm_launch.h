@@ -31,10 +31,9 @@ cudaError_t launch_bits_from_list(const int64_t* cells, int64_t n, int nz, int r
 
 cudaError_t launch_fluid_interior(const StepArgs& A, bool q16, bool force, bool special, bool dither,
                                   int qmode, cudaStream_t st);
-// D3Q19 interior step (two-chain moment-space streaming; fp32, or q16 with the default
-// QuantSpec -- qmode 2); other D3Q19 codecs use the per-cell kernel (pull_cells mode 3)
+// D3Q19 interior step (two-chain moment-space streaming; fp32, or q16 with any codec mode)
 cudaError_t launch_fluid_interior19(const StepArgs& A, bool q16, bool force, bool special, bool dither,
-                                    cudaStream_t st);
+                                    int qmode, cudaStream_t st);
 // mode 0: voxel bounce-back on masked links; 1: reset listed solid cells to rest;
 // 2: triangle mesh, Eq.-8 boundary populations on masked links (t table in A.cut_t);
 // 3: fused single-kernel step over all cells with a dense per-cell mask (Alg. 1 baseline)

@@ -417,3 +417,27 @@ def test_per_component_errors(case):
         print(f"{case} {n:4s} plane-rel {pl:.2e}  moment-rel {mo:.2e}  maxabs/range {mx:.2e}")
     assert max(v[1] for v in ce.values()) <= FP32_TOL
     assert max(v[2] for v in ce.values()) <= FP32_TOL
+
+
+@pytest.mark.parametrize("quant", ["14/13", "12/11", "custom16"])
+def test_d3q19_interior_non_default_codecs(quant):
+    """D3Q19 with a bit preset or custom 16-bit ranges runs the two-chain interior kernel (codec
+    modes 0 / 1) -- it matches the per-cell D3Q19 kernel and the oracle's quantized step within 1 LSB."""
+    from oracle import lattice as OL
+    q = (QuantSpec(mmin=(0.9,) + QuantSpec().mmin[1:], mmax=(1.2,) + QuantSpec().mmax[1:]) if quant == "custom16"
+         else QuantSpec.preset(quant))
+    shape = (12, 20, 36)
+    state = OS.random_state(shape, seed=5, drho=0.04, umax=0.05, sneq=0.004)
+    mn, mx, bits = np.array(q.mmin), np.array(q.mmax), np.array(q.bits)
+    w0, _ = codec.encode_state(state[0], state[1], neq_decompose(*state), mn, mx, bits)
+    cfg = SolverConfig(nu=0.02, precision="q16", quant=q, lattice="D3Q19")
+    res = {}
+    for kind in ("interior", "per_cell"):
+        with Solver(SimGrid(shape), cfg) as s:
+            s.codes = w0
+            s.step(1) if kind == "interior" else s.step_percell(1)
+            res[kind] = s.codes
+    ref, _ = OS.fluid_step_q16(w0, cfg.tau, 0, mmin=mn, mmax=mx, bits=bits, lat=OL.D3Q19)
+    for kind, w in res.items():
+        d = np.abs(codec.unpack(w).astype(np.int64) - codec.unpack(ref).astype(np.int64))
+        assert d.max() <= 1, (kind, d.max())
