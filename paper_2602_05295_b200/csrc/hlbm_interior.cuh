@@ -580,10 +580,10 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
   int item = blockIdx.x;
+  const int xsi = item / (g.nzt * g.nyt);
+  item -= xsi * (g.nzt * g.nyt);
   const int zt = item % g.nzt;
-  item /= g.nzt;
-  const int yt = item % g.nyt;
-  const int xsi = item / g.nyt;
+  const int yt = item / g.nzt;
   const int zs0 = zt * kZT;                 // storage column of the window start
   const int y0 = yt * kRows;                // first interior row; the box starts at storage row y0
   const int yrow = y0 + w - 1;              // logical y of this warp's row (row warps 1..15)
