@@ -258,24 +258,34 @@ def _dist_env():
     return world, rank, local
 
 
-def _make(precision, world, rank, local, gnx=None):
+def _make(precision, world, rank, local, gnx=None, scene="box"):
     """Weak scaling (default): (512 N) x 512 x 512, the same field on every slab.  Strong scaling
-    (gnx given): gnx x 512 x 512 split into N x-slabs."""
+    (gnx given): gnx x 512 x 512 split into N x-slabs.  scene "vehicle"
+    (SURVEY §8d configs 4/5): the procedural vehicle scaled to the global grid, inflow / outflow in
+    x, periodic y / z, u_in = 0.1, nu = 1e-5, 16-bit with dither (fp32 beside)."""
     from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
-    from paper_2602_05295_b200.geometry import turbulence_modes
-    cfg = SolverConfig(nu=1e-4, precision=precision, quant=QuantSpec(), device=local)
+    from paper_2602_05295_b200.geometry import turbulence_modes, vehicle_mask
     gnx = N_PER_GPU * world if gnx is None else gnx
     gdims = (gnx, N_PER_GPU, N_PER_GPU)
-    modes = turbulence_modes(N_PER_GPU, seed=0)
-    modes = modes.copy()
-    modes[:, 0] *= gnx // N_PER_GPU   # wave numbers along x scale with the global nx
+    mask = None
+    if scene == "vehicle":
+        cfg = SolverConfig(nu=1e-5, precision=precision, quant=QuantSpec(dither=precision == "q16"), device=local,
+                           bc={"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("periodic", "periodic")},
+                           u_in=(0.1, 0.0, 0.0))
+        modes = np.array([[0, 0, 0, 0.1, 0.0, 0.0, np.pi / 2]])   # uniform u_in
+        mask = vehicle_mask(gdims, seed=0)
+    else:
+        cfg = SolverConfig(nu=1e-4, precision=precision, quant=QuantSpec(), device=local)
+        modes = turbulence_modes(N_PER_GPU, seed=0)
+        modes = modes.copy()
+        modes[:, 0] *= gnx // N_PER_GPU   # wave numbers along x scale with the global nx
     if world > 1:
         from paper_2602_05295_b200.distributed import DistributedSolver
-        ds = DistributedSolver(gdims, cfg)
+        ds = DistributedSolver(gdims, cfg, mask=mask)
         ds.solver.init_modes(modes)
         return ds, ds.solver
     import torch
-    s = Solver(SimGrid(gdims), cfg)
+    s = Solver(SimGrid(gdims, mask), cfg)
     s.set_stream(torch.cuda.current_stream().cuda_stream)
     s.init_modes(modes)
     return None, s
@@ -382,7 +392,7 @@ def run_ours(args):
     results = {}
     e2e = None
     for precision in ("q16", "fp32"):
-        ds, s = _make(precision, world, rank, local, gnx if strong else None)
+        ds, s = _make(precision, world, rank, local, gnx if strong else None, args.scene)
         with ClockSampler(local) as clk:
             ms, launches = _timed(ds, s, args.steps, args.warmup, world)
         cells = (gnx // world) * N_PER_GPU * N_PER_GPU      # this rank's slab
@@ -421,11 +431,16 @@ def run_ours(args):
         "metric": METRIC, "value": round(head["value"], 1), "unit": "MLUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4),
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: solenoidal random Fourier modes 1<=|k|<=4, u_rms=0.05, seed 0",
-        "config": {"workload": ("SURVEY config 5 (strong scaling): periodic fluid-only turbulence box "
-                                f"{STRONG_NX}x512x512 in x-slabs, 16-bit moments (fp32 measured beside)") if strong else
-                               ("BASELINE configs[1]: periodic fluid-only turbulence box, 16-bit moments "
-                                "(fp32 measured beside)"),
+        "data": ("synthetic: procedural vehicle mask (geometry.vehicle_mask, seed 0), uniform inflow u = 0.1"
+                 if args.scene == "vehicle" else "synthetic: solenoidal random Fourier modes 1<=|k|<=4, u_rms=0.05, seed 0"),
+        "config": {"workload": (("SURVEY config 5 (strong scaling): " + (
+                                   "procedural vehicle, inflow/outflow, 16-bit + dither" if args.scene == "vehicle"
+                                   else "periodic fluid-only turbulence box") +
+                                f" {STRONG_NX}x512x512 in x-slabs (fp32 measured beside)") if strong else
+                               ("BASELINE configs[4]-style weak scaling: procedural vehicle over (512 N)x512x512, "
+                                "16-bit + dither (fp32 beside)" if args.scene == "vehicle" else
+                                "BASELINE configs[1]: periodic fluid-only turbulence box, 16-bit moments "
+                                "(fp32 measured beside)")),
                    "grid_per_gpu": [gnx // world, N_PER_GPU, N_PER_GPU], "global_grid": [gnx, N_PER_GPU, N_PER_GPU],
                    "nu": 1e-4, "precision": "q16", "parallelism": f"x-slab dp{world}",
                    "l2": f"inputs larger than L2: {2 * 20 * (gnx // world) * N_PER_GPU ** 2 / 1e9:.1f} GB (q16) / "
@@ -504,6 +519,8 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scene", default="box", choices=["box", "vehicle"],
+                    help="box: periodic turbulence box (BASELINE configs[1]); vehicle: obstacle scene (configs 4/5)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: 2048x512x512 global grid split over the GPUs (default: weak, 512^3 per GPU)")
     args = ap.parse_args()
