@@ -55,17 +55,30 @@ def step_key(step: int, seed: int) -> int:
                                & 0xFFFFFFFF)))
 
 
+DITHER_MULT = (0x9E3779B1, 0x85EBCA77, 0xC2B2AE3D, 0x27D4EB2F)   # odd multipliers, words 1..4
+
+
+def dither_words(h0):
+    """The 5 noise words of a cell from its hash h0: word 0 = h0, word k = m ^ (m >> 16) with
+    m = h0 * M_k mod 2^32 (a bijection of h0 for every k, so each word is uniform when h0 is)."""
+    h0 = _u32(h0)
+    out = [h0]
+    for mk in DITHER_MULT:
+        m = (h0 * np.uint64(mk)) & np.uint64(0xFFFFFFFF)
+        out.append(m ^ (m >> np.uint64(16)))
+    return out
+
+
 def dither_noise(cell_index, step: int, seed: int) -> np.ndarray:
     """Noise in LSB units, shape (10, ...) for global linear cell indices.
 
-    h0 = mix32(cell + key(step, seed)); word k hash h_k = mix32(h0 ^ (k+1)*0x9E3779B9);
-    component 2k takes the low 16 bits, 2k+1 the high 16 bits;
+    h0 = mix32(cell + key(step, seed)); the 5 words come from ``dither_words(h0)``;
+    component 2k takes the low 16 bits of word k, 2k+1 the high 16 bits;
     noise = bits/65536 - 1/2 (exact in float32 and float64)."""
     cell = np.asarray(cell_index, dtype=np.uint64)
     h0 = mix32(cell + np.uint64(step_key(step, seed)))
     out = []
-    for k in range(NWORDS):
-        hk = mix32(h0 ^ np.uint64(((k + 1) * 0x9E3779B9) & 0xFFFFFFFF))
+    for hk in dither_words(h0):
         lo = (hk & np.uint64(0xFFFF)).astype(np.float64)
         hi = (hk >> np.uint64(16)).astype(np.float64)
         out.append(lo / 65536.0 - 0.5)

@@ -159,7 +159,7 @@ __device__ __forceinline__ void store_cell(const StepArgs& A, int x, int y, int 
       const uint32_t h0 = mix32(gi + A.step_key);
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
-        const uint32_t h = mix32(h0 ^ ((uint32_t)(k + 1) * 0x9E3779B9u));
+        const uint32_t h = dither_word(h0, k);
         nz[2 * k] = noise16(h & 0xFFFFu);
         nz[2 * k + 1] = noise16(h >> 16);
       }

@@ -494,8 +494,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
       const uint32_t h0a = mix32(gi + A.step_key), h0b = mix32(gi + 1u + A.step_key);
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
-        const uint32_t kk = (uint32_t)(k + 1) * 0x9E3779B9u;
-        const uint32_t ha = mix32(h0a ^ kk), hb = mix32(h0b ^ kk);
+        const uint32_t ha = dither_word(h0a, k), hb = dither_word(h0b, k);
         nz[2 * k] = make_float2(noise16(ha & 0xFFFFu), noise16(hb & 0xFFFFu));
         nz[2 * k + 1] = make_float2(noise16(ha >> 16), noise16(hb >> 16));
       }

@@ -330,6 +330,14 @@ __host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16;
   return x;
 }
+// noise word k of a cell from its hash h0 (oracle/codec.py dither_words): word 0 = h0, word k =
+// m ^ (m >> 16) with m = h0 * M_k -- one IMAD + one shift-xor instead of a full mix32 per word
+__device__ __forceinline__ uint32_t dither_word(uint32_t h0, int k) {
+  constexpr uint32_t M[4] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du, 0x27D4EB2Fu};
+  if (k == 0) return h0;
+  const uint32_t m = h0 * M[k - 1];
+  return m ^ (m >> 16);
+}
 // 16 noise bits -> bits/65536 - 1/2 exactly: float(1 + bits/2^16) - 1.5
 __device__ __forceinline__ float noise16(uint32_t bits16) {
   return __uint_as_float(0x3F800000u | (bits16 << 7)) - 1.5f;

@@ -125,6 +125,16 @@ def test_dither_unbiased():
     sigma = step / np.sqrt(12)
     assert abs(err.mean()) < 3 * sigma / np.sqrt(cells.size)
     assert np.all(noise >= -0.5) and np.all(noise < 0.5)
+    # every component's noise is zero-mean uniform (std 1/sqrt(12)) and the components of a cell
+    # are uncorrelated (words 1..4 are multiply-xorshift bijections of the cell hash)
+    n = noise.reshape(10, -1)
+    assert np.all(np.abs(n.mean(axis=1)) < 4 / np.sqrt(12 * n.shape[1]))
+    assert np.allclose(n.std(axis=1), 1 / np.sqrt(12), rtol=2e-3)
+    c = np.corrcoef(n)
+    assert np.abs(c - np.eye(10)).max() < 5e-3
+    # and neighbouring cells / steps are uncorrelated
+    assert abs(np.corrcoef(n[0, :-1], n[0, 1:])[0, 1]) < 5e-3
+    assert abs(np.corrcoef(n[0], codec.dither_noise(cells, 4, 11)[0])[0, 1]) < 5e-3
 
 
 def test_saturation_counts_exact():
