@@ -76,18 +76,46 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        # NVML (the library nvidia-smi reads), opened here -- outside the timed region -- and polled
+        # every 10 ms, so a 35 ms timed region still gets several samples; else nvidia-smi / 100 ms
+        self._nvml = None
+        try:
+            import pynvml as nvml
+            nvml.nvmlInit()
+            vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+            phys = int(vis[index]) if len(vis) > index and vis[index].strip().isdigit() else index
+            self._h = nvml.nvmlDeviceGetHandleByIndex(phys)   # NVML counts physical devices
+            self._mx = nvml.nvmlDeviceGetMaxClockInfo(self._h, nvml.NVML_CLOCK_SM)
+            self._bits = [nvml.nvmlClocksThrottleReasonHwSlowdown, nvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                          nvml.nvmlClocksThrottleReasonSwThermalSlowdown, nvml.nvmlClocksThrottleReasonSwPowerCap]
+            self._nvml = nvml
+        except Exception:
+            self._nvml = None
 
     def _run(self):
+        nvml = self._nvml
+        if nvml is not None:
+            h, mx, bits = self._h, self._mx, self._bits
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if nvml is not None:
+                    sm = nvml.nvmlDeviceGetClockInfo(h, nvml.NVML_CLOCK_SM)
+                    r = nvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.01 if nvml is not None else 0.1)
+        if nvml is not None:
+            try:
+                nvml.nvmlShutdown()
+            except Exception:
+                pass
 
     def __enter__(self):
         self._t.start()
