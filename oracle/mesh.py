@@ -63,11 +63,13 @@ def segment_triangle(o, d, v0, v1, v2):
     return hit, t
 
 
-def cut_links(vertices, faces, dims):
-    """Earliest hit per (node, direction) of every pull link x -> x - c_i.
+def cut_links(vertices, faces, dims, lat=None):
+    """Earliest hit per (node, direction) of every pull link x -> x - c_i (directions of ``lat``:
+    D3Q27 by default, D3Q19 tests its 18 links only).
 
     Returns (cells int64 sorted, masks uint32, t float64 (n, 27) with NaN where uncut,
     tri int64 (n, 27) with -1 where uncut)."""
+    lat = lat or L.D3Q27
     V = np.asarray(vertices, dtype=np.float64)
     F = np.asarray(faces, dtype=np.int64)
     nx, ny, nz = dims
@@ -87,8 +89,8 @@ def cut_links(vertices, faces, dims):
         X, Y, Z = np.meshgrid(xs, ys, zs, indexing="ij")
         X, Y, Z = X.ravel(), Y.ravel(), Z.ravel()
         o = (X.astype(np.float64), Y.astype(np.float64), Z.astype(np.float64))
-        for i in range(1, L.Q):
-            cx, cy, cz = (float(-v) for v in L.C[i])
+        for i in range(1, lat.Q):
+            cx, cy, cz = (float(-v) for v in lat.C[i])
             d = (np.full(X.shape, cx), np.full(X.shape, cy), np.full(X.shape, cz))
             hit, t = segment_triangle(o, d, tuple(p0), tuple(p1), tuple(p2))
             for j in np.nonzero(hit)[0]:
@@ -101,8 +103,8 @@ def cut_links(vertices, faces, dims):
     cells = np.array(sorted({c for c, _ in best_t}), dtype=np.int64)
     index = {c: n for n, c in enumerate(cells.tolist())}
     masks = np.zeros(len(cells), dtype=np.uint32)
-    tt = np.full((len(cells), L.Q), np.nan)
-    tri = np.full((len(cells), L.Q), -1, dtype=np.int64)
+    tt = np.full((len(cells), 27), np.nan)
+    tri = np.full((len(cells), 27), -1, dtype=np.int64)
     for (c, i), tv in best_t.items():
         n = index[c]
         masks[n] |= np.uint32(1 << i)
@@ -111,16 +113,18 @@ def cut_links(vertices, faces, dims):
     return cells, masks, tt, tri
 
 
-def step_with_mesh(rho, mom, stress, tau, cells, t, solid=None, force=None):
-    """One periodic fluid step with the Eq.-8 boundary populations on cut links.
+def step_with_mesh(rho, mom, stress, tau, cells, t, solid=None, force=None, lat=None):
+    """One periodic fluid step with the Eq.-8 boundary populations on cut links (``lat``: D3Q27
+    default, or D3Q19).
 
     ``solid`` = (v, omega, center) of the rigid body (zero by default).  Returns
     (rho, mom, stress, F_solid, T_solid)."""
     nx, ny, nz = rho.shape
     v, om, cen = (np.zeros(3), np.zeros(3), np.zeros(3)) if solid is None else (np.asarray(a, float) for a in solid)
+    lat = lat or L.D3Q27
     r, m, s = collide_moments(rho, mom, stress, force, tau)                    # collision.py:137
-    f = reconstruct_distributions(r, m, s)                                       # moments.py:64
-    fs = np.stack([np.roll(f[i], shift=tuple(L.C[i]), axis=(0, 1, 2)) for i in range(L.Q)])
+    f = reconstruct_distributions(r, m, s, lat)                                  # moments.py:64
+    fs = np.stack([np.roll(f[i], shift=tuple(lat.C[i]), axis=(0, 1, 2)) for i in range(lat.Q)])
     Fs = np.zeros(3)
     Ts = np.zeros(3)
     for n, cell in enumerate(cells.tolist()):
@@ -129,22 +133,22 @@ def step_with_mesh(rho, mom, stress, tau, cells, t, solid=None, force=None):
         rx = r[x, y, z]
         ux = m[:, x, y, z] / rx
         sx = s[:, x, y, z] / rx
-        for i in range(1, L.Q):
+        for i in range(1, lat.Q):
             if not np.isfinite(t[n, i]):
                 continue
-            c = L.C[i].astype(np.float64)
+            c = lat.C[i].astype(np.float64)
             p = np.array([x, y, z], dtype=np.float64) - t[n, i] * c
             up = v + np.cross(om, p - cen)
             # S_p = u_p u_p + (S_x - u_x u_x)   (Eq. 8), Voigt order xx xy xz yy yz zz
             pairs = ((0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2))
             sp = np.array([up[a] * up[b] + (sx[k] - ux[a] * ux[b]) for k, (a, b) in enumerate(pairs)])
-            fp = reconstruct_distributions(np.array([rx]), (rx * up)[:, None], (rx * sp)[:, None])[i, 0]
+            fp = reconstruct_distributions(np.array([rx]), (rx * up)[:, None], (rx * sp)[:, None], lat)[i, 0]
             df = fp - fs[i, x, y, z]
             fs[i, x, y, z] = fp
             dP = -df * c
             Fs += dP
             Ts += np.cross(p - cen, dP)
-    r2, m2, s2 = moments_from_distributions(fs)                                 # moments.py:25
+    r2, m2, s2 = moments_from_distributions(fs, lat)                            # moments.py:25
     return r2, m2, s2, Fs, Ts
 
 

@@ -289,7 +289,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   if (cnt > 0) {
     StepArgs Am = A;
     Am.cut_t = ctx->mesh.t32 + a * 27;
-    CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, st));
+    CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, st, ctx->q));
     ++ctx->launches;
   }
   return fix_one_row(ctx, xb, xr, st);
@@ -786,7 +786,6 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
   for (int64_t k = 0; k < 3 * nv; ++k)
     if (!std::isfinite(vertices[k])) return fail(ctx, HLBM_EINVAL, "non-finite vertex");
   const hlbm_config& c = ctx->cfg;
-  if (ctx->q != 27) return fail(ctx, HLBM_EINVAL, "triangle meshes need the D3Q27 lattice");
   // the mesh replaces any voxel lists
   cudaFree(ctx->d_fused); ctx->d_fused = nullptr;
   cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
@@ -809,7 +808,7 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
     CK(cudaMalloc(&dF, (size_t)3 * nf * 4));
     CK(cudaMemcpy(dV, V.data(), V.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dF, faces, (size_t)3 * nf * 4, cudaMemcpyHostToDevice));
-    CK(build_mesh_links(dV, dF, (int)nf, c.nx, c.ny, c.nz, ctx->mesh, ctx->stream));
+    CK(build_mesh_links(dV, dF, (int)nf, c.nx, c.ny, c.nz, ctx->mesh, ctx->stream, ctx->q));
     cudaFree(dV);
     cudaFree(dF);
   }
@@ -978,7 +977,7 @@ int hlbm_step_reference(hlbm_ctx* ctx, int32_t nsteps) {
       ++ctx->launches;
     }
     if (ctx->mesh.nb) {
-      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream));
+      CK(launch_pull_cells(A, ctx->mesh.cells, ctx->mesh.masks, ctx->mesh.nb, 2, q16, force, dither, ctx->stream, ctx->q));
       ++ctx->launches;
     }
     ctx->cur = 1 - ctx->cur;

@@ -104,7 +104,7 @@ __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z
                                           r * ux * uy + mc.nxy, r * ux * uz + mc.nxz, r * uy * uy + mc.nyy,
                                           r * uy * uz + mc.nyz, r * uz * uz + mc.nzz);
     float Ep, Op;
-    eval_eo<cx, cy, cz, float>(Cp, Ep, Op);
+    eval_eo<cx, cy, cz, float, Q>(Cp, Ep, Op);
     const float fp = Ep + Op;
     // momentum exchange: Delta P = -(f_p - f_streamed) c_i on the solid
     const float df = fp - ft;
@@ -519,8 +519,8 @@ cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uin
     if (q == 19) {                                                                                           \
       if (mode == 0) pull_cells<QQ, F, D, 0, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);      \
       else if (mode == 1) pull_cells<QQ, F, D, 1, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
-      else if (mode == 3) pull_cells<QQ, F, D, 3, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
-      else return cudaErrorInvalidValue;                                                                     \
+      else if (mode == 2) pull_cells<QQ, F, D, 2, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
+      else pull_cells<QQ, F, D, 3, 19><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);                  \
     } else if (mode == 0) pull_cells<QQ, F, D, 0, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base); \
     else if (mode == 1) pull_cells<QQ, F, D, 1, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);   \
     else if (mode == 2) pull_cells<QQ, F, D, 2, 27><<<(unsigned)nb, tpb, 0, st>>>(A, cells, masks, n, base);   \

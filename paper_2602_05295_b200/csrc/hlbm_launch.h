@@ -24,7 +24,7 @@ struct MeshLinks {               // cut-link table of a static triangle mesh (de
   int64_t nb = 0;
 };
 cudaError_t build_mesh_links(const double* dV, const int* dF, int nf, int nx, int ny, int nz, MeshLinks& out,
-                             cudaStream_t st);
+                             cudaStream_t st, int q = 27);
 
 cudaError_t launch_bits_from_list(const int64_t* cells, int64_t n, int nz, int row_words, uint32_t* bits,
                                   cudaStream_t st);

@@ -64,6 +64,7 @@ __device__ __forceinline__ double seg_tri(D3 o, D3 d, D3 v0, D3 v1, D3 v2) {
 
 struct MeshGeo {
   int nx, ny, nz;
+  int q;   // velocity set: links 1 .. q-1 are tested (27 or 19)
 };
 
 __device__ __forceinline__ bool tri_box(const double* V, const int* F, int k, MeshGeo g, int lo[3], int hi[3]) {
@@ -108,10 +109,11 @@ __global__ void intersect(const double* __restrict__ V, const int* __restrict__ 
     const D3 v1 = {V[3 * F[3 * k + 1]], V[3 * F[3 * k + 1] + 1], V[3 * F[3 * k + 1] + 2]};
     const D3 v2 = {V[3 * F[3 * k + 2]], V[3 * F[3 * k + 2] + 1], V[3 * F[3 * k + 2] + 2]};
     const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
-    const int64_t work = (int64_t)ex * ey * ez * 26;
+    const int nl = g.q - 1;
+    const int64_t work = (int64_t)ex * ey * ez * nl;
     for (int64_t w = lane; w < work; w += 32) {
-      const int i = 1 + (int)(w % 26);
-      const int64_t node = w / 26;
+      const int i = 1 + (int)(w % nl);
+      const int64_t node = w / nl;
       const int z = lo[2] + (int)(node % ez), y = lo[1] + (int)((node / ez) % ey), x = lo[0] + (int)(node / ((int64_t)ez * ey));
       const D3 o = {(double)x, (double)y, (double)z};
       const D3 d = {(double)-mCX[i], (double)-mCY[i], (double)-mCZ[i]};
@@ -128,10 +130,10 @@ __global__ void intersect(const double* __restrict__ V, const int* __restrict__ 
 
 // per candidate: link mask, class flag (bit 0 = has a cut link)
 __global__ void finalize_candidates(const unsigned long long* __restrict__ tkey, int64_t m,
-                                    uint32_t* __restrict__ masks, uint8_t* __restrict__ flag) {
+                                    uint32_t* __restrict__ masks, uint8_t* __restrict__ flag, int q) {
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x) {
     uint32_t mk = 0;
-    for (int i = 1; i < 27; ++i)
+    for (int i = 1; i < q; ++i)
       if (tkey[c * 27 + i] != ~0ull) mk |= 1u << i;
     masks[c] = mk;
     flag[c] = mk ? 1 : 0;
@@ -174,8 +176,8 @@ static unsigned grid_of(int64_t n, int tpb) {
 }
 
 cudaError_t build_mesh_links(const double* dV, const int* dF, int nf, int nx, int ny, int nz, MeshLinks& out,
-                             cudaStream_t st) {
-  const MeshGeo g{nx, ny, nz};
+                             cudaStream_t st, int q) {
+  const MeshGeo g{nx, ny, nz, q};
   const int64_t n = (int64_t)nx * ny * nz;
   uint8_t* mark = nullptr;
   int* idx = nullptr;
@@ -216,7 +218,7 @@ cudaError_t build_mesh_links(const double* dV, const int* dF, int nf, int nx, in
     MK(cudaMemsetAsync(tri, 0x7F, m * 27 * 4, st));
     for (int pass = 0; pass < 2; ++pass)
       intersect<<<grid_of((int64_t)nf * 32, 256), 256, 0, st>>>(dV, dF, nf, g, idx, tkey, tri, pass);
-    finalize_candidates<<<grid_of(m, 256), 256, 0, st>>>(tkey, m, cmask, flag);
+    finalize_candidates<<<grid_of(m, 256), 256, 0, st>>>(tkey, m, cmask, flag, q);
     // compact the candidates that carry a cut link (candidate order = cell order)
     const int64_t nt2 = compact_tiles(m);
     int64_t* counts2 = nullptr;
