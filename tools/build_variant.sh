@@ -7,7 +7,7 @@ cd "$(dirname "$0")/../paper_2602_05295_b200/csrc"
 out=../../variants/$name; mkdir -p $out
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --extended-lambda -Xcompiler -fPIC"
 objs=""
-for f in hlbm_interior hlbm_interior_q0 hlbm_interior_q1 hlbm_interior_q2 hlbm_interior_q19 hlbm_interior_q19m hlbm_cells hlbm_mesh hlbm_capi; do
+for f in hlbm_interior hlbm_interior_q0 hlbm_interior_q1 hlbm_interior_q2 hlbm_interior_q19 hlbm_interior_q19m hlbm_cells hlbm_pull_f32 hlbm_pull_q16 hlbm_alg1 hlbm_mesh hlbm_capi; do
   nvcc $FL "$@" -c $f.cu -o $out/$f.o & objs="$objs $out/$f.o"
 done
 wait

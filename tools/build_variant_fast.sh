@@ -11,7 +11,7 @@ nvcc $FL "$@" -c hlbm_interior.cu -o $out/hlbm_interior.o &
 nvcc $FL "$@" -c hlbm_interior_q2.cu -o $out/hlbm_interior_q2.o &
 wait
 objs="$out/hlbm_interior.o $out/hlbm_interior_q2.o"
-for f in hlbm_interior_q0 hlbm_interior_q1 hlbm_interior_q19 hlbm_interior_q19m hlbm_cells hlbm_mesh hlbm_capi; do objs="$objs build/$f.o"; done
+for f in hlbm_interior_q0 hlbm_interior_q1 hlbm_interior_q19 hlbm_interior_q19m hlbm_cells hlbm_pull_f32 hlbm_pull_q16 hlbm_alg1 hlbm_mesh hlbm_capi; do objs="$objs build/$f.o"; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libhlbm.so $objs -lcudart
 rm -f $out/*.o
 echo built $out/libhlbm.so
