@@ -119,3 +119,31 @@ def test_fused_split_half_step_equivalence(case, steps):
     err = rel(split, ref, fl)
     print(case, f"split(n) vs S(fused(n)), n = {steps}:", err)
     assert max(err) <= TOL, err
+
+
+@pytest.mark.parametrize("case", ["periodic", "channel_sphere"])
+def test_alg1_d3q19_and_equivalence(case):
+    """The original kernel on the D3Q19 lattice (19-link reconstruction and streaming, D3Q19
+    weights) against the oracle's C o S, and the half-step equivalence with the D3Q19 split step."""
+    from oracle import lattice as OL
+    shape = (16, 20, 24)
+    mask = sphere_mask(shape, (7, 9.5, 11.5), 3) if case == "channel_sphere" else None
+    bc = CHANNEL if mask is not None else None
+    kw = {"bc": bc, "u_in": (0.05, 0, 0)} if bc else {}
+    cfg = SolverConfig(nu=0.02, lattice="D3Q19", **kw)
+    obc = OS.BC(x=bc["x"], y=bc["y"], z=bc["z"], u_in=(0.05, 0, 0)) if bc else OS.BC()
+    m0 = _post_state(shape, 8, mask)
+    with Solver(SimGrid(shape, mask), cfg) as s:
+        s.set_moments(*m0)
+        s.step_fused(5)
+        fused = s.moments()
+    ref = m0
+    for _ in range(5):
+        ref = OS.alg1_step(*ref, cfg.tau, obc, None, mask, OL.D3Q19)
+    fl = None if mask is None else ~mask.astype(bool)
+    assert max(rel(fused, ref, fl)) <= TOL
+    with Solver(SimGrid(shape, mask), cfg) as s:
+        s.set_moments(*OS.stream_step(*m0, obc, mask, OL.D3Q19))
+        s.step(5)
+        split = s.moments()
+    assert max(rel(split, OS.stream_step(*fused, obc, mask, OL.D3Q19), fl)) <= TOL
