@@ -786,6 +786,10 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
   for (int64_t k = 0; k < 3 * nv; ++k)
     if (!std::isfinite(vertices[k])) return fail(ctx, HLBM_EINVAL, "non-finite vertex");
   const hlbm_config& c = ctx->cfg;
+  for (int f = 0; f < 6; ++f)
+    if (c.bc[f] == HLBM_BC_WALL)   // (round 1 dropped the wall lists here silently)
+      return fail(ctx, HLBM_EINVAL, "triangle meshes with wall faces are not supported (the wall links live in "
+                                    "the voxel boundary lists, which the mesh replaces); use a voxel mask");
   // the mesh replaces any voxel lists
   cudaFree(ctx->d_fused); ctx->d_fused = nullptr;
   cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
