@@ -11,6 +11,8 @@
                       bit-for-bit resume point
   StepStats CSV       step, t_fluid_ms, t_copy_ms, t_solid_ms, mass, momentum_x/y/z, max_u,
                       saturation_0..9                                              -- SPEC.md:531
+  vorticity PGM       binary P5 of omega_z = d u_y/dx - d u_x/dy (central differences) on one z
+                      slice, linear map of [-range, range] onto 0..255          -- SPEC.md:510
 """
 
 from __future__ import annotations
@@ -123,3 +125,24 @@ class StatsCSV:
 
     def __exit__(self, *a):
         self.close()
+
+
+def vorticity_z(velocity, z=None):
+    """omega_z = d u_y / dx - d u_x / dy by periodic central differences on one z slice (default: the
+    middle) of a (3, nx, ny, nz) velocity field -> (nx, ny) float64 (SPEC.md:510, 2-D flows)."""
+    u = np.asarray(velocity, dtype=np.float64)
+    k = u.shape[3] // 2 if z is None else int(z)
+    ux, uy = u[0, :, :, k], u[1, :, :, k]
+    return 0.5 * (np.roll(uy, -1, axis=0) - np.roll(uy, 1, axis=0)) - 0.5 * (np.roll(ux, -1, axis=1) - np.roll(ux, 1, axis=1))
+
+
+def write_vorticity_pgm(path, velocity, vrange, z=None):
+    """Optional PGM vorticity image of a snapshot: omega_z of one z slice mapped linearly
+    from [-vrange, vrange] onto grey levels 0..255 (clipped), binary P5, rows = y (top = ny - 1), columns = x."""
+    w = vorticity_z(velocity, z)
+    g = np.clip(np.rint((w / float(vrange) + 1.0) * 127.5), 0, 255).astype(np.uint8)
+    img = np.ascontiguousarray(g.T[::-1])   # (ny, nx), y up
+    with open(path, "wb") as f:
+        f.write(f"P5\n{img.shape[1]} {img.shape[0]}\n255\n".encode("ascii"))
+        f.write(img.tobytes())
+    return w

@@ -58,3 +58,21 @@ def test_checkpoint_resume_bitwise(tmp_path, precision):
         assert hio.load_checkpoint(tmp_path / "c.hlbm", b) == 4
         b.step(5)
         assert np.array_equal(b.get_state(), ref)
+
+
+def test_vorticity_pgm(tmp_path):
+    from paper_2602_05295_b200.io import vorticity_z, write_vorticity_pgm
+    n = 32
+    k = 2 * np.pi / n
+    x = np.arange(n)[:, None, None]
+    y = np.arange(n)[None, :, None]
+    u = np.zeros((3, n, n, 4))
+    u[0] = np.sin(k * y) * np.ones((1, 1, 4))          # shear u_x(y): omega_z = -du_x/dy = -k cos(ky)
+    w = vorticity_z(u)
+    np.testing.assert_allclose(w, -np.sin(k) * np.cos(k * y[:, :, 0]) * np.ones((n, 1)), atol=1e-12)
+    p = tmp_path / "w.pgm"
+    write_vorticity_pgm(p, u, vrange=2 * np.sin(k))
+    data = p.read_bytes()
+    assert data.startswith(b"P5\n32 32\n255\n") and len(data) == len(b"P5\n32 32\n255\n") + n * n
+    img = np.frombuffer(data[len(b"P5\n32 32\n255\n"):], dtype=np.uint8).reshape(n, n)
+    assert img.min() >= 63 and img.max() <= 192          # |omega| <= vrange / 2 -> the middle half
