@@ -113,18 +113,35 @@ def cut_links(vertices, faces, dims, lat=None):
     return cells, masks, tt, tri
 
 
-def step_with_mesh(rho, mom, stress, tau, cells, t, solid=None, force=None, lat=None):
-    """One periodic fluid step with the Eq.-8 boundary populations on cut links (``lat``: D3Q27
-    default, or D3Q19).
+def step_with_mesh(rho, mom, stress, tau, cells, t, solid=None, force=None, lat=None, bc=None):
+    """One fluid step with the Eq.-8 boundary populations on cut links (``lat``: D3Q27 default, or
+    D3Q19).  ``bc`` (oracle.step.BC, default periodic): domain faces; links into a wall face take
+    the half-way bounce-back population, which wins over a mesh hit on the same link.
 
     ``solid`` = (v, omega, center) of the rigid body (zero by default).  Returns
     (rho, mom, stress, F_solid, T_solid)."""
     nx, ny, nz = rho.shape
     v, om, cen = (np.zeros(3), np.zeros(3), np.zeros(3)) if solid is None else (np.asarray(a, float) for a in solid)
     lat = lat or L.D3Q27
-    r, m, s = collide_moments(rho, mom, stress, force, tau)                    # collision.py:137
-    f = reconstruct_distributions(r, m, s, lat)                                  # moments.py:64
-    fs = np.stack([np.roll(f[i], shift=tuple(lat.C[i]), axis=(0, 1, 2)) for i in range(lat.Q)])
+    wall = None
+    if bc is None:
+        r, m, s = collide_moments(rho, mom, stress, force, tau)                # collision.py:137
+        f = reconstruct_distributions(r, m, s, lat)                              # moments.py:64
+        fs = np.stack([np.roll(f[i], shift=tuple(lat.C[i]), axis=(0, 1, 2)) for i in range(lat.Q)])
+    else:
+        from . import step as OS
+        padded = OS.pad_state(rho, mom, stress, bc)
+        rp, mp, sp_ = collide_moments(padded[0], padded[1:4], padded[4:10], force, tau)
+        fpad = reconstruct_distributions(rp, mp, sp_, lat)
+        fs = np.stack([fpad[i, 1 - cx:1 - cx + nx, 1 - cy:1 - cy + ny, 1 - cz:1 - cz + nz]
+                       for i, (cx, cy, cz) in enumerate(lat.C)])
+        f = fpad[:, 1:-1, 1:-1, 1:-1]
+        r, m, s = rp[1:-1, 1:-1, 1:-1], mp[:, 1:-1, 1:-1, 1:-1], sp_[:, 1:-1, 1:-1, 1:-1]
+        wall = OS.link_masks_dense(np.zeros((nx, ny, nz), dtype=bool), bc, lat)
+        for i in range(1, lat.Q):
+            sel = ((wall >> np.uint32(i)) & np.uint32(1)).astype(bool)
+            if sel.any():
+                fs[i][sel] = f[lat.OPP[i]][sel]
     Fs = np.zeros(3)
     Ts = np.zeros(3)
     for n, cell in enumerate(cells.tolist()):
@@ -136,6 +153,8 @@ def step_with_mesh(rho, mom, stress, tau, cells, t, solid=None, force=None, lat=
         for i in range(1, lat.Q):
             if not np.isfinite(t[n, i]):
                 continue
+            if wall is not None and (int(wall[x, y, z]) >> i) & 1:
+                continue                                   # the wall wins: bounce-back already set
             c = lat.C[i].astype(np.float64)
             p = np.array([x, y, z], dtype=np.float64) - t[n, i] * c
             up = v + np.cross(om, p - cen)

@@ -158,6 +158,7 @@ StepArgs make_args(hlbm_ctx* ctx, int with_stats, int xb = 0, int xr = -1) {
   A.do_stats = with_stats;
   A.stats = ctx->d_stats;
   A.cut_t = ctx->mesh.t32;
+  A.wall_masks = ctx->mesh.wmasks;
   for (int k = 0; k < 3; ++k) {
     A.solid_v[k] = ctx->solid_v[k];
     A.solid_w[k] = ctx->solid_w[k];
@@ -199,6 +200,7 @@ void free_mesh(hlbm_ctx* ctx) {
   cudaFree(ctx->mesh.t64);
   cudaFree(ctx->mesh.t32);
   cudaFree(ctx->mesh.tri);
+  cudaFree(ctx->mesh.wmasks);
   ctx->mesh = MeshLinks();
 }
 
@@ -289,6 +291,7 @@ int run_range(hlbm_ctx* ctx, int xb, int xr, int with_stats, cudaEvent_t after_i
   if (cnt > 0) {
     StepArgs Am = A;
     Am.cut_t = ctx->mesh.t32 + a * 27;
+    Am.wall_masks = ctx->mesh.wmasks ? ctx->mesh.wmasks + a : nullptr;
     CK(launch_pull_cells(Am, ctx->mesh.cells + a, ctx->mesh.masks + a, cnt, 2, q16, force, dither, st, ctx->q));
     ++ctx->launches;
   }
@@ -786,10 +789,23 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
   for (int64_t k = 0; k < 3 * nv; ++k)
     if (!std::isfinite(vertices[k])) return fail(ctx, HLBM_EINVAL, "non-finite vertex");
   const hlbm_config& c = ctx->cfg;
-  for (int f = 0; f < 6; ++f)
-    if (c.bc[f] == HLBM_BC_WALL)   // (round 1 dropped the wall lists here silently)
-      return fail(ctx, HLBM_EINVAL, "triangle meshes with wall faces are not supported (the wall links live in "
-                                    "the voxel boundary lists, which the mesh replaces); use a voxel mask");
+  // wall faces: their links come from the voxel classifier on an all-fluid mask (round 1 dropped
+  // them here silently); the list becomes the union of mesh-cut and wall-adjacent cells
+  std::vector<int64_t> wcells;
+  std::vector<uint32_t> wmasks;
+  bool wall = false;
+  for (int f = 0; f < 6; ++f) wall = wall || c.bc[f] == HLBM_BC_WALL;
+  if (wall) {
+    const int64_t pl = (int64_t)c.ny * c.nz;
+    std::vector<uint8_t> zero((size_t)(pl * c.nx), 0);
+    if (int r = hlbm_set_mask(ctx, zero.data(), zero.data(), zero.data())) return r;
+    wcells.resize((size_t)ctx->nb);
+    wmasks.resize((size_t)ctx->nb);
+    if (ctx->nb) {
+      CK(cudaMemcpy(wcells.data(), ctx->d_bcells, ctx->nb * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(wmasks.data(), ctx->d_bmasks, ctx->nb * 4, cudaMemcpyDeviceToHost));
+    }
+  }
   // the mesh replaces any voxel lists
   cudaFree(ctx->d_fused); ctx->d_fused = nullptr;
   cudaFree(ctx->d_bcells); ctx->d_bcells = nullptr;
@@ -816,6 +832,54 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
     cudaFree(dV);
     cudaFree(dF);
   }
+  if (!wcells.empty()) {   // merge the wall-adjacent cells into the (sorted) cut-link list
+    const int64_t nm = ctx->mesh.nb;
+    std::vector<int64_t> mc((size_t)nm);
+    std::vector<uint32_t> mm((size_t)nm);
+    std::vector<double> mt((size_t)nm * 27);
+    std::vector<int> mtri((size_t)nm * 27);
+    if (nm) {
+      CK(cudaMemcpy(mc.data(), ctx->mesh.cells, nm * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(mm.data(), ctx->mesh.masks, nm * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(mt.data(), ctx->mesh.t64, nm * 27 * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(mtri.data(), ctx->mesh.tri, nm * 27 * 4, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int64_t> uc;
+    std::vector<uint32_t> um, uw;
+    std::vector<double> ut;
+    std::vector<int> utri;
+    size_t i = 0, j = 0;
+    while (i < mc.size() || j < wcells.size()) {
+      const bool takem = j >= wcells.size() || (i < mc.size() && mc[i] <= wcells[j]);
+      const bool takew = i >= mc.size() || (j < wcells.size() && wcells[j] <= mc[i]);
+      uc.push_back(takem ? mc[i] : wcells[j]);
+      um.push_back(takem ? mm[i] : 0u);
+      uw.push_back(takew ? wmasks[j] : 0u);
+      for (int k = 0; k < 27; ++k) {
+        ut.push_back(takem ? mt[i * 27 + k] : std::nan(""));
+        utri.push_back(takem ? mtri[i * 27 + k] : -1);
+      }
+      if (takem) ++i;
+      if (takew) ++j;
+    }
+    free_mesh(ctx);
+    const int64_t nu = (int64_t)uc.size();
+    std::vector<float> ut32(ut.size());
+    for (size_t k = 0; k < ut.size(); ++k) ut32[k] = (float)ut[k];
+    CK(cudaMalloc(&ctx->mesh.cells, nu * 8));
+    CK(cudaMalloc(&ctx->mesh.masks, nu * 4));
+    CK(cudaMalloc(&ctx->mesh.wmasks, nu * 4));
+    CK(cudaMalloc(&ctx->mesh.t64, nu * 27 * 8));
+    CK(cudaMalloc(&ctx->mesh.t32, nu * 27 * 4));
+    CK(cudaMalloc(&ctx->mesh.tri, nu * 27 * 4));
+    CK(cudaMemcpy(ctx->mesh.cells, uc.data(), nu * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->mesh.masks, um.data(), nu * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->mesh.wmasks, uw.data(), nu * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->mesh.t64, ut.data(), nu * 27 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->mesh.t32, ut32.data(), nu * 27 * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->mesh.tri, utri.data(), nu * 27 * 4, cudaMemcpyHostToDevice));
+    ctx->mesh.nb = nu;
+  }
   ctx->off_b.clear();
   ctx->off_s.clear();
   if (int r = plane_offsets(ctx, ctx->mesh.cells, ctx->mesh.nb, ctx->off_m)) return r;
@@ -832,6 +896,38 @@ int hlbm_set_mesh(hlbm_ctx* ctx, const double* vertices, int64_t nv, const int32
 
 int hlbm_get_cut_links(hlbm_ctx* ctx, int64_t* cells, uint32_t* masks, double* t, int32_t* tri, int64_t* n) {
   if (!ctx || !n) return fail(ctx, HLBM_EINVAL, "null argument");
+  if (ctx->mesh.wmasks) {   // union list (mesh + wall faces): report the mesh-cut entries only
+    const int64_t nu = ctx->mesh.nb;
+    std::vector<int64_t> uc((size_t)nu);
+    std::vector<uint32_t> um((size_t)nu);
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (nu) {
+      CK(cudaMemcpy(uc.data(), ctx->mesh.cells, nu * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(um.data(), ctx->mesh.masks, nu * 4, cudaMemcpyDeviceToHost));
+    }
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < nu; ++i) cnt += um[(size_t)i] != 0;
+    if (!cells) { *n = cnt; return HLBM_OK; }
+    if (*n < cnt) return fail(ctx, HLBM_EINVAL, "output buffer too small");
+    *n = cnt;
+    std::vector<double> ut((size_t)nu * 27);
+    std::vector<int> utri((size_t)nu * 27);
+    if (nu && t) CK(cudaMemcpy(ut.data(), ctx->mesh.t64, nu * 27 * 8, cudaMemcpyDeviceToHost));
+    if (nu && tri) CK(cudaMemcpy(utri.data(), ctx->mesh.tri, nu * 27 * 4, cudaMemcpyDeviceToHost));
+    const int64_t off = (int64_t)ctx->cfg.x0 * ctx->cfg.ny * ctx->cfg.nz;
+    int64_t o = 0;
+    for (int64_t i = 0; i < nu; ++i) {
+      if (!um[(size_t)i]) continue;
+      cells[o] = uc[(size_t)i] + off;
+      if (masks) masks[o] = um[(size_t)i];
+      for (int k = 0; k < 27; ++k) {
+        if (t) t[o * 27 + k] = ut[(size_t)i * 27 + k];
+        if (tri) tri[o * 27 + k] = utri[(size_t)i * 27 + k];
+      }
+      ++o;
+    }
+    return HLBM_OK;
+  }
   const int64_t nb = ctx->mesh.nb;
   if (!cells) { *n = nb; return HLBM_OK; }
   CK(cudaStreamSynchronize(ctx->stream));

@@ -48,6 +48,7 @@ __device__ __forceinline__ void load_cell(const StepArgs& A, int sp, int y, int 
 struct MeshCtx {
   float rho, d, nxx, nxy, nxz, nyy, nyz, nzz;   // neq part of rho S+ at x: X - j+ j+ / rho
   const float* t;                               // this cell's 27 hit parameters
+  uint32_t wmask;                                // links into a wall face (bounce-back, wins over the mesh)
   float F[3], T[3];                              // momentum exchange accumulators
 };
 
@@ -72,8 +73,9 @@ __device__ __forceinline__ void pull_link(const StepArgs& A, int x, int y, int z
                                           float m[10], MeshCtx& mc) {
   constexpr int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
   const Geo& g = A.g;
-  const bool cut = (mask >> I) & 1u;
-  const bool bb = MODE == 0 && cut;
+  const bool wcut = MODE == 2 && ((mc.wmask >> I) & 1u);   // wall face: half-way bounce-back
+  const bool cut = ((mask >> I) & 1u) && !wcut;
+  const bool bb = (MODE == 0 && cut) || wcut;
   const int sx = bb ? x : x - cx;
   const int sy = bb ? y : y - cy;   // ghost rows/columns hold the periodic images
   const int sz = bb ? z : z - cz;
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(128) pull_cells(const __grid_constant__ StepAr
         mc.nxx = P.Xxx - P.jpx * P.ux; mc.nxy = P.Xxy - P.jpx * P.uy; mc.nxz = P.Xxz - P.jpx * P.uz;
         mc.nyy = P.Xyy - P.jpy * P.uy; mc.nyz = P.Xyz - P.jpy * P.uz; mc.nzz = P.Xzz - P.jpz * P.uz;
         mc.t = A.cut_t + idx * 27;
+        mc.wmask = A.wall_masks ? A.wall_masks[idx] : 0u;
       }
       float m[10];
 #pragma unroll

@@ -21,6 +21,8 @@ struct MeshLinks {               // cut-link table of a static triangle mesh (de
   double* t64 = nullptr;         // (nb, 27) hit parameter, NaN where uncut (exported)
   float* t32 = nullptr;          // (nb, 27) the same in float for the step kernel
   int* tri = nullptr;            // (nb, 27) triangle index, -1 where uncut
+  uint32_t* wmasks = nullptr;    // with wall faces: bit i = the link crosses a wall (bounce-back; the
+                                 // list is then the union of mesh-cut and wall-adjacent cells)
   int64_t nb = 0;
 };
 cudaError_t build_mesh_links(const double* dV, const int* dF, int nf, int nx, int ny, int nz, MeshLinks& out,

@@ -73,6 +73,7 @@ struct StepArgs {
   int do_stats;
   Stats* stats;
   const float* cut_t;               // mesh mode: (n_list, 27) hit parameters t (p = x - t c_i)
+  const uint32_t* wall_masks;       // mesh mode with wall faces: per list entry, links into a wall
   float solid_v[3], solid_w[3], solid_c[3];   // rigid-body velocity, angular velocity, centre
 };
 

@@ -214,9 +214,7 @@ def test_range_split_step_bitwise(precision, mesh):
     from oracle.mesh import icosphere
     gshape = (40, 24, 32)
     mask = sphere_mask(gshape, (20, 11.5, 15.5), 6)
-    # triangle meshes and wall faces do not combine (hlbm_set_mesh rejects it): z periodic there
-    bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"),
-          "z": ("periodic", "periodic") if mesh else ("wall", "wall")}
+    bc = {"x": ("inflow", "outflow"), "y": ("periodic", "periodic"), "z": ("wall", "wall")}
     cfg = SolverConfig(nu=0.02, bc=bc, u_in=(0.05, 0, 0), precision=precision,
                        quant=QuantSpec(dither=True), seed=3)
     state = _sphere_state(gshape, mask)
@@ -264,15 +262,3 @@ def test_distributed_solver_single_rank_overlap_path():
     finally:
         ds.solver.close()
     assert np.array_equal(got, ref)
-
-
-
-def test_mesh_with_wall_faces_is_rejected():
-    """Wall faces need the voxel boundary lists, which a triangle mesh replaces: the combination is
-    an explicit ValueError (round 1 dropped the walls silently)."""
-    from oracle.mesh import icosphere
-    cfg = SolverConfig(nu=0.02, bc={"z": ("wall", "wall")})
-    with Solver(SimGrid((16, 16, 16)), cfg) as s:
-        v, f = icosphere((8, 8, 8), 3.0, 1)
-        with pytest.raises(ValueError, match="wall"):
-            s.set_mesh(v, f)
