@@ -71,8 +71,8 @@ def main():
         run("2 turbulence box", (512, 512, 512), SolverConfig(nu=1e-4, precision=prec),
             lambda s: s.init_modes(turbulence_modes(512)))
     uniform = lambda u: (lambda s: s.init_modes(np.array([[0, 0, 0, u, 0, 0, np.pi / 2]])))
-    # D3Q27 vs D3Q19 at the paper's 720x360x360 comparison size; D3Q19 runs on
-    # the per-cell fused kernel (one thread per cell gathering its 19 sources)
+    # D3Q27 vs D3Q19 at the paper's 720x360x360 comparison size; D3Q19 runs the
+    # two-chain interior kernel (216 w = prod(4,1,1) + prod(2,-1,-1))
     for lat in ("D3Q27", "D3Q19"):
         run(f"lattice {lat} 720x360x360 box", (720, 360, 360), SolverConfig(nu=1e-4, precision="q16", lattice=lat),
             lambda s: s.init_modes(turbulence_modes(360, dims=(720, 360, 360))), steps=20)
