@@ -1,4 +1,5 @@
-"""Install the B200 solver into the reference package's namespace as ``momentlbm.solver``.
+"""Install the B200 solver into the reference package's namespace as ``momentlbm.solver`` (and the
+obstacle-geometry module ``momentlbm.geometry``).
 
 The reference package (/root/reference/pkg, installed unmodified into baseline/_ref) lists
 ``momentlbm.solver`` in its layout (pkg/src/momentlbm/__init__.py:1-9) but does not ship it.

@@ -148,3 +148,30 @@ def test_run_zero_steps_is_the_initial_snapshot():
     assert len(res.snapshots) == 1 and res.snapshots[0].step == 0 and res.stats == []
     assert np.all(res.snapshots[0].rho == 1.0)
     res.grid.close()
+
+
+def test_geometry_module_in_the_reference_namespace(tmp_path):
+    """momentlbm.geometry (SPEC.md:388-444): load_mesh, link_intersect, voxelize_surface, with the
+    SPEC examples, and the surface mask covers every node the GPU cut-link finder (same test) cuts."""
+    dropin.install()
+    import momentlbm.geometry as G
+    from oracle import mesh as M
+    p = tmp_path / "tri.obj"
+    p.write_text("v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 3\n")
+    m = G.load_mesh(p)
+    assert m.vertices.shape == (3, 3) and m.faces.tolist() == [[0, 1, 2]]
+    # axis link crossing a perpendicular triangle at its midpoint -> t = 0.5
+    tri = np.array([[0.5, -1.0, -1.0], [0.5, 3.0, -1.0], [0.5, -1.0, 3.0]])
+    t, hit = G.link_intersect((1.0, 0.0, 0.0), (1, 0, 0), tri)
+    assert t == pytest.approx(0.5) and np.allclose(hit, (0.5, 0, 0))
+    # parallel / coplanar link -> no hit
+    assert G.link_intersect((0.5, 0.0, 0.0), (0, 1, 0), tri) is None
+    # SurfaceMask covers the nodes with cut links
+    V, F = M.icosphere((10.3, 9.7, 11.1), 4.2, 2)
+    dims = (22, 20, 24)
+    mask = G.voxelize_surface(G.TriangleMesh(V, F), dims)
+    cells, _, _, _ = M.cut_links(V, F, dims)
+    x, r = np.divmod(cells, dims[1] * dims[2])
+    y, z = np.divmod(r, dims[2])
+    assert mask[x, y, z].all()
+    assert mask.sum() < 0.25 * mask.size
