@@ -175,3 +175,30 @@ def test_geometry_module_in_the_reference_namespace(tmp_path):
     y, z = np.divmod(r, dims[2])
     assert mask[x, y, z].all()
     assert mask.sum() < 0.25 * mask.size
+
+
+@pytest.mark.gpu
+def test_solver_with_mesh_obstacle_and_solid_state():
+    """A TriangleMesh with a SolidState as a momentlbm.solver obstacle: the step applies Eq. 8 with
+    the body's velocity (oracle mesh step with the same motion)."""
+    from oracle import mesh as M
+    from oracle import step as OS
+    _, S = _mods()
+    import momentlbm.geometry as G
+    shape = (24, 20, 28)
+    V, F = M.icosphere((11.3, 9.7, 13.9), 5.2, 2)
+    motion = ((0.01, -0.005, 0.0), (0.0, 0.002, 0.001), (11.3, 9.7, 13.9))
+    mesh = G.TriangleMesh(V, F, G.SolidState(*motion))
+    cfg = S.SolverConfig(nu=0.02, obstacles=[mesh])
+    state = OS.random_state(shape, seed=5, drho=0.02, umax=0.04, sneq=0.002)
+    g = S.SimGrid(shape)
+    g.set_moments(*state)
+    S.fluid_update_step(g, cfg)
+    S.solid_correction_step(g, cfg)
+    got = g.moments()
+    cells, _, t, _ = M.cut_links(V, F, shape)
+    r, m, sx, Fs, _ = M.step_with_mesh(*state, cfg.tau, cells, t, solid=motion)
+    for a, b in zip(got, (r, m, sx)):
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
+    np.testing.assert_allclose(g.last_stats.force, Fs, rtol=1e-4, atol=1e-7)
+    g.close()
