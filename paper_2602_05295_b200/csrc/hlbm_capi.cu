@@ -413,13 +413,18 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
     ctx->RG.mx[k] = mx;
     ctx->RG.levels[k] = L;
     const double shift = (k == 0) ? 1.0 : 0.0;   // component 0 is held as d = rho - 1
-    ctx->Q.dec_step[k] = (float)((mx - mn) / L);
-    ctx->Q.dec_off[k] = (float)(mn - shift);
-    ctx->dec_step_d[k] = (mx - mn) / L;
-    ctx->dec_off_d[k] = mn - shift;
+    // decode re-centred on q0 = the code of the centre value (hlbm_math.cuh Codec::dec_c)
+    const double step = (mx - mn) / L;
+    const double q0 = ctx->q16 ? std::min(L, std::max(0.0, std::floor((shift - mn) / step + 0.5))) : 0.0;
+    ctx->Q.dec_step[k] = (float)step;
+    ctx->Q.dec_off[k] = (float)(mn - shift + q0 * step);
+    ctx->Q.dec_c[k] = (float)(8388608.0 + q0);
+    ctx->dec_step_d[k] = step;
+    ctx->dec_off_d[k] = mn - shift + q0 * step;
     const double sc = L / (mx - mn);
     ctx->Q.enc_scale[k] = (float)sc;
     ctx->Q.enc_off[k] = (float)((shift - mn) * sc + 0.5);
+    ctx->Q.enc_nb[k] = (float)(-1.5 + 1.0 / 131072.0 - ((double)ctx->Q.enc_off[k] - ((shift - mn) * sc + 0.5)));
     const double mid = 0.5 * (mn + mx), half = 0.5 * (mx - mn);
     ctx->Q.sat_a[k] = (float)(1.0 / half);
     ctx->Q.sat_b[k] = (float)((shift - mid) / half);

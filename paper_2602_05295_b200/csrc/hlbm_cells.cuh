@@ -38,8 +38,8 @@ __device__ __forceinline__ void load_cell(const StepArgs& A, int sp, int y, int 
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       const uint32_t wv = __ldg(p + k * g.cstride);
-      s[2 * k] = __fmaf_rn(code_lo_f(wv) - 8388608.0f, A.Q.dec_step[2 * k], A.Q.dec_off[2 * k]);
-      s[2 * k + 1] = __fmaf_rn(code_hi_f(wv) - 8388608.0f, A.Q.dec_step[2 * k + 1], A.Q.dec_off[2 * k + 1]);
+      s[2 * k] = __fmaf_rn(code_lo_f(wv) - A.Q.dec_c[2 * k], A.Q.dec_step[2 * k], A.Q.dec_off[2 * k]);
+      s[2 * k + 1] = __fmaf_rn(code_hi_f(wv) - A.Q.dec_c[2 * k + 1], A.Q.dec_step[2 * k + 1], A.Q.dec_off[2 * k + 1]);
     }
   }
 }
@@ -154,15 +154,15 @@ __device__ __forceinline__ void store_cell(const StepArgs& A, int x, int y, int 
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
         const uint32_t h = dither_word(h0, k);
-        nz[2 * k] = noise16(h & 0xFFFFu);
-        nz[2 * k + 1] = noise16(h >> 16);
+        nz[2 * k] = noise16u(h & 0xFFFFu) + A.Q.enc_nb[2 * k];
+        nz[2 * k + 1] = noise16u(h >> 16) + A.Q.enc_nb[2 * k + 1];
       }
     }
     uint32_t code[10];
 #pragma unroll
     for (int c = 0; c < 10; ++c) {
       float t = __fmaf_rn(s[c], A.Q.enc_scale[c], A.Q.enc_off[c]);
-      if (DITHER) t += nz[c];
+      if (DITHER) t = __fadd_rd(t, nz[c]);   // hlbm_math.cuh noise16u
       code[c] = min(f2u16_floor(t), A.Q.levels[c]);
       const float r = __fmaf_rn(s[c], A.Q.sat_a[c], A.Q.sat_b[c]);
       if (stat && !(fabsf(r) <= 1.0f)) atomicAdd(&A.stats->sat[c], 1ull);

@@ -341,11 +341,22 @@ __device__ __forceinline__ void yx_stage(V (*exch)[kNW][32], int wu, int wd, int
 struct DefQ {
   __host__ __device__ static constexpr double mn(int c) { return c == 0 ? 0.8 : (c < 4 ? -0.6 : -0.1); }
   __host__ __device__ static constexpr double mx(int c) { return c == 0 ? 1.5 : (c < 4 ? 0.6 : 0.1); }
-  __host__ __device__ static constexpr float dec_step(int c) { return (float)((mx(c) - mn(c)) / 65535.0); }
-  __host__ __device__ static constexpr float dec_off(int c) { return (float)(mn(c) - (c == 0 ? 1.0 : 0.0)); }
+  __host__ __device__ static constexpr double step_d(int c) { return (mx(c) - mn(c)) / 65535.0; }
+  __host__ __device__ static constexpr double q0(int c) {   // code of the centre (rho = 1, else 0)
+    return (double)(long long)(((c == 0 ? 1.0 : 0.0) - mn(c)) / step_d(c) + 0.5);
+  }
+  __host__ __device__ static constexpr float dec_step(int c) { return (float)step_d(c); }
+  __host__ __device__ static constexpr float dec_off(int c) {   // re-centred (Codec::dec_c)
+    return (float)(mn(c) - (c == 0 ? 1.0 : 0.0) + q0(c) * step_d(c));
+  }
+  __host__ __device__ static constexpr float dec_c(int c) { return (float)(8388608.0 + q0(c)); }
   __host__ __device__ static constexpr float enc_scale(int c) { return (float)(65535.0 / (mx(c) - mn(c))); }
-  __host__ __device__ static constexpr float enc_off(int c) {
-    return (float)(((c == 0 ? 1.0 : 0.0) - mn(c)) * (65535.0 / (mx(c) - mn(c))) + 0.5);
+  __host__ __device__ static constexpr double enc_off_d(int c) {
+    return ((c == 0 ? 1.0 : 0.0) - mn(c)) * (65535.0 / (mx(c) - mn(c))) + 0.5;
+  }
+  __host__ __device__ static constexpr float enc_off(int c) { return (float)enc_off_d(c); }
+  __host__ __device__ static constexpr float enc_nb(int c) {   // Codec::enc_nb
+    return (float)(-1.5 + 1.0 / 131072.0 - ((double)enc_off(c) - enc_off_d(c)));
   }
 };
 template <int QMODE> __device__ __forceinline__ float q_dec_step(const Codec& Q, int c) {
@@ -353,6 +364,12 @@ template <int QMODE> __device__ __forceinline__ float q_dec_step(const Codec& Q,
 }
 template <int QMODE> __device__ __forceinline__ float q_dec_off(const Codec& Q, int c) {
   return QMODE == 2 ? DefQ::dec_off(c) : Q.dec_off[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_dec_c(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::dec_c(c) : Q.dec_c[c];
+}
+template <int QMODE> __device__ __forceinline__ float q_enc_nb(const Codec& Q, int c) {
+  return QMODE == 2 ? DefQ::enc_nb(c) : Q.enc_nb[c];
 }
 template <int QMODE> __device__ __forceinline__ float q_enc_scale(const Codec& Q, int c) {
   return QMODE == 2 ? DefQ::enc_scale(c) : Q.enc_scale[c];
@@ -378,25 +395,23 @@ __device__ __forceinline__ void load_state(const uint32_t (*st)[kBoxRows][kZW], 
       if (PRE) s[c] = vmul(s[c], A.pre_k[c]);
     }
   } else if (PRE) {
-    const V two23 = vsplat(8388608.0f);
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       const uint2 wv = *reinterpret_cast<const uint2*>(&st[k][row][2 * lane]);
       const V lo = make_float2(code_lo_f(wv.x), code_lo_f(wv.y));
       const V hi = make_float2(code_hi_f(wv.x), code_hi_f(wv.y));
-      s[2 * k] = vfma(vsub(lo, two23), vsplat(A.pre_step[2 * k]), vsplat(A.pre_off[2 * k]));
-      s[2 * k + 1] = vfma(vsub(hi, two23), vsplat(A.pre_step[2 * k + 1]), vsplat(A.pre_off[2 * k + 1]));
+      s[2 * k] = vfma(vsub(lo, vsplat(q_dec_c<QMODE>(A.Q, 2 * k))), vsplat(A.pre_step[2 * k]), vsplat(A.pre_off[2 * k]));
+      s[2 * k + 1] = vfma(vsub(hi, vsplat(q_dec_c<QMODE>(A.Q, 2 * k + 1))), vsplat(A.pre_step[2 * k + 1]), vsplat(A.pre_off[2 * k + 1]));
     }
   } else {
-    const V two23 = vsplat(8388608.0f);
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       const uint2 wv = *reinterpret_cast<const uint2*>(&st[k][row][2 * lane]);
       const V lo = make_float2(code_lo_f(wv.x), code_lo_f(wv.y));
       const V hi = make_float2(code_hi_f(wv.x), code_hi_f(wv.y));
-      s[2 * k] = vfma(vsub(lo, two23), vsplat(q_dec_step<QMODE>(A.Q, 2 * k)),
+      s[2 * k] = vfma(vsub(lo, vsplat(q_dec_c<QMODE>(A.Q, 2 * k))), vsplat(q_dec_step<QMODE>(A.Q, 2 * k)),
                       vsplat(q_dec_off<QMODE>(A.Q, 2 * k)));
-      s[2 * k + 1] = vfma(vsub(hi, two23), vsplat(q_dec_step<QMODE>(A.Q, 2 * k + 1)),
+      s[2 * k + 1] = vfma(vsub(hi, vsplat(q_dec_c<QMODE>(A.Q, 2 * k + 1))), vsplat(q_dec_step<QMODE>(A.Q, 2 * k + 1)),
                           vsplat(q_dec_off<QMODE>(A.Q, 2 * k + 1)));
     }
   }
@@ -495,8 +510,10 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
         const uint32_t ha = dither_word(h0a, k), hb = dither_word(h0b, k);
-        nz[2 * k] = make_float2(noise16(ha & 0xFFFFu), noise16(hb & 0xFFFFu));
-        nz[2 * k + 1] = make_float2(noise16(ha >> 16), noise16(hb >> 16));
+        nz[2 * k] = vadd(make_float2(noise16u(ha & 0xFFFFu), noise16u(hb & 0xFFFFu)),
+                         vsplat(q_enc_nb<QMODE>(A.Q, 2 * k)));
+        nz[2 * k + 1] = vadd(make_float2(noise16u(ha >> 16), noise16u(hb >> 16)),
+                             vsplat(q_enc_nb<QMODE>(A.Q, 2 * k + 1)));
       }
     }
     V t[10];
@@ -547,7 +564,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     }
     if (DITHER) {
 #pragma unroll
-      for (int c = 0; c < 10; ++c) t[c] = vadd(t[c], nz[c]);
+      for (int c = 0; c < 10; ++c) t[c] = vadd_rd(t[c], nz[c]);
     }
     uint2 wd[5];
 #pragma unroll

@@ -24,6 +24,7 @@ namespace hlbm {
 typedef float2 V;
 __device__ __forceinline__ V vsplat(float s) { return make_float2(s, s); }
 __device__ __forceinline__ V vadd(V a, V b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ V vadd_rd(V a, V b) { return __fadd2_rd(a, b); }
 __device__ __forceinline__ V vsub(V a, V b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 __device__ __forceinline__ V vmul(V a, V b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ V vmul(V a, float s) { return __fmul2_rn(a, vsplat(s)); }
@@ -306,9 +307,17 @@ __device__ __forceinline__ void raw_to_state(const T m[10], T out[10], T* inv_ou
 // exact float of q.  For component 0 the kernel decodes d = rho - 1 directly (min - 1).
 struct Codec {
   float dec_step[10];   // (max-min)/(2^b-1)
-  float dec_off[10];    // min (component 0: min - 1)
+  float dec_off[10];    // decode offset, re-centred: (min - shift) + q0 * step  (see dec_c)
+  float dec_c[10];      // 2^23 + q0, q0 = the code of the range's centre value (rho = 1, else 0):
+                        // v = (float(2^23 + q) - dec_c) * step + dec_off -- the subtraction is exact
+                        // and the offset small, so the fp32 decode carries no systematic bias
+                        // (with min - shift as the offset it was -1e-8 (d) / -4e-8 (j) per cell,
+                        // a linear mass / momentum drift over long dithered runs)
   float enc_scale[10];  // (2^b-1)/(max-min)
   float enc_off[10];    // -min*scale + 1/2   (component 0: -(min-1)*scale + 1/2)
+  float enc_nb[10];     // dither offset: noise = u + enc_nb, u = 1 + bits/2^16 in [1, 2);
+                        // -3/2 + 2^-17 (zero-mean noise) - (float(enc_off) - enc_off) (the
+                        // offset's fp32 rounding), so that E[code] is the exact scaled value
   float sat_a[10];      // r = m*sat_a + sat_b, saturated iff |r| > 1
   float sat_b[10];
   uint32_t levels[10];  // 2^b - 1
@@ -339,9 +348,11 @@ __device__ __forceinline__ uint32_t dither_word(uint32_t h0, int k) {
   return m ^ (m >> 16);
 }
 // 16 noise bits -> bits/65536 - 1/2 exactly: float(1 + bits/2^16) - 1.5
-__device__ __forceinline__ float noise16(uint32_t bits16) {
-  return __uint_as_float(0x3F800000u | (bits16 << 7)) - 1.5f;
-}
+// 1 + bits16 / 2^16 in [1, 2); the dither noise is this + Codec::enc_nb, added to t with
+// round-down (vadd_rd) so that floor(t + noise) is the floor of the exact sum -- a round-to-nearest
+// add lifts sums within half an ulp (2^-9..2^-8 LSB at t ~ 2^15) below an integer onto it, a
+// +2^-10..2^-9 LSB bias of every dithered code (a steady mass / momentum drift)
+__device__ __forceinline__ float noise16u(uint32_t bits16) { return __uint_as_float(0x3F800000u | (bits16 << 7)); }
 
 // floor, saturating to [0, 2^32-1] (negative and NaN -> 0); callers clamp to 2^b - 1
 __device__ __forceinline__ uint32_t f2u16_floor(float t) {
