@@ -286,7 +286,7 @@ def _dist_env():
     return world, rank, local
 
 
-def _make(precision, world, rank, local, gnx=None, scene="box"):
+def _make(precision, world, rank, local, gnx=None, scene="box", halo="p2p"):
     """Weak scaling (default): (512 N) x 512 x 512, the same field on every slab.  Strong scaling
     (gnx given): gnx x 512 x 512 split into N x-slabs.  scene "vehicle"
     (SURVEY §8d configs 4/5): the procedural vehicle scaled to the global grid, inflow / outflow in
@@ -309,7 +309,7 @@ def _make(precision, world, rank, local, gnx=None, scene="box"):
         modes[:, 0] *= gnx // N_PER_GPU   # wave numbers along x scale with the global nx
     if world > 1:
         from paper_2602_05295_b200.distributed import DistributedSolver
-        ds = DistributedSolver(gdims, cfg, mask=mask)
+        ds = DistributedSolver(gdims, cfg, mask=mask, transport=halo)
         ds.solver.init_modes(modes)
         return ds, ds.solver
     import torch
@@ -420,7 +420,7 @@ def run_ours(args):
     results = {}
     e2e = None
     for precision in ("q16", "fp32"):
-        ds, s = _make(precision, world, rank, local, gnx if strong else None, args.scene)
+        ds, s = _make(precision, world, rank, local, gnx if strong else None, args.scene, args.halo)
         with ClockSampler(local) as clk:
             ms, launches = _timed(ds, s, args.steps, args.warmup, world)
         cells = (gnx // world) * N_PER_GPU * N_PER_GPU      # this rank's slab
@@ -448,6 +448,7 @@ def run_ours(args):
         if precision == "q16":
             e2e = _e2e(ds, s, world, max(args.steps, 200))
         if ds is not None:
+            ds.close()
             ds.solver.close()
         else:
             s.close()
@@ -471,6 +472,8 @@ def run_ours(args):
                                 "(fp32 measured beside)")),
                    "grid_per_gpu": [gnx // world, N_PER_GPU, N_PER_GPU], "global_grid": [gnx, N_PER_GPU, N_PER_GPU],
                    "nu": 1e-4, "precision": "q16", "parallelism": f"x-slab dp{world}",
+                   "halo": ("none" if world == 1 else
+                            "CUDA IPC peer store" if args.halo == "ipc" else "torch.distributed P2P (NCCL)"),
                    "l2": f"inputs larger than L2: {2 * 20 * (gnx // world) * N_PER_GPU ** 2 / 1e9:.1f} GB (q16) / "
                          f"{2 * 40 * (gnx // world) * N_PER_GPU ** 2 / 1e9:.1f} GB (fp32) of double-buffered state "
                          "per GPU vs 126 MB L2"},
@@ -551,6 +554,9 @@ def main():
                     help="box: periodic turbulence box (BASELINE configs[1]); vehicle: obstacle scene (configs 4/5)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: 2048x512x512 global grid split over the GPUs (default: weak, 512^3 per GPU)")
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "ipc"],
+                    help="N > 1: halo planes as NCCL send/recv (p2p) or stored into the neighbours' ghost "
+                         "planes through CUDA IPC mappings (ipc, DESIGN.md §7)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

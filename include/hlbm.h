@@ -172,6 +172,26 @@ int hlbm_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_
  * schedule sends a step's edge planes while the bulk of that step is still being computed */
 int hlbm_next_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
                           int64_t* bytes);
+/* peer-store halo between processes: instead of a send/receive
+ * pair, each rank copies its freshly written edge planes straight into its neighbours' ghost
+ * planes through CUDA IPC mappings (NVLink peer memory across GPUs).
+ *   hlbm_ipc_export : the cudaIpcMemHandle_t of both state buffers (2 x 64 bytes) and the
+ *                     current buffer index, to be passed to the neighbours
+ *   hlbm_ipc_open   : map a neighbour's buffers; side 0 = the x-lo neighbour, 1 = x-hi;
+ *                     peer_nx = its interior planes, peer_cur = its current buffer index
+ *   hlbm_ipc_sync   : re-align after a rank replaced its state (its current index changed)
+ *   hlbm_halo_push  : enqueue on `cuda_stream` (NULL: the context's) the copies of our first /
+ *                     last interior plane -- of the buffer the step in progress writes when
+ *                     next_buffer, else of the current one -- into the lo / hi neighbour's hi / lo
+ *                     ghost plane of the matching buffer.  The caller orders it against the
+ *                     neighbours' steps (interprocess events; paper_2602_05295_b200/distributed.py)
+ *   hlbm_ipc_close  : unmap (also done by hlbm_destroy)
+ * The reference has no multi-GPU path; this replaces nothing there. */
+int hlbm_ipc_export(hlbm_ctx* ctx, void* handles, int32_t* cur);
+int hlbm_ipc_open(hlbm_ctx* ctx, int32_t side, const void* handles, int32_t peer_nx, int32_t peer_cur);
+int hlbm_ipc_sync(hlbm_ctx* ctx, int32_t side, int32_t peer_cur);
+int hlbm_halo_push(hlbm_ctx* ctx, int32_t next_buffer, void* cuda_stream);
+int hlbm_ipc_close(hlbm_ctx* ctx);
 /* one step split into x-ranges (edge planes first, bulk later): step_begin resets
  * the statistics when with_stats, step_range enqueues the interior + boundary kernels for the
  * destination planes [x_begin, x_end) of the slab, step_end makes the written buffer current.

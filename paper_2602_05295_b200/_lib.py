@@ -85,6 +85,11 @@ SIGNATURES = {
                                    C.POINTER(C.c_int64)]),
     "hlbm_next_halo_planes": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                                         C.POINTER(C.c_int64)]),
+    "hlbm_ipc_export": (C.c_int, [_P, _P, C.POINTER(C.c_int32)]),
+    "hlbm_ipc_open": (C.c_int, [_P, C.c_int32, _P, C.c_int32, C.c_int32]),
+    "hlbm_ipc_sync": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "hlbm_halo_push": (C.c_int, [_P, C.c_int32, C.c_void_p]),
+    "hlbm_ipc_close": (C.c_int, [_P]),
     "hlbm_step_begin": (C.c_int, [_P, C.c_int32]),
     "hlbm_step_range": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "hlbm_step_range_on": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_void_p]),

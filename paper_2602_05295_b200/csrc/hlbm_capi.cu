@@ -59,6 +59,15 @@ struct hlbm_ctx {
   int64_t steps = 0;
   int64_t launches = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // peer-store halo (hlbm_ipc_*): the x-lo (0) and x-hi (1) neighbours' state buffers mapped
+  // through CUDA IPC; a neighbour's current buffer is (our cur) ^ rel -- every rank flips its
+  // buffer once per step, so the relation holds until a rank re-imports its state
+  struct Peer {
+    void* buf[2] = {nullptr, nullptr};
+    int nx = 0, rel = 0;
+    bool open = false, owner = false;
+    cudaIpcMemHandle_t h[2];
+  } peer[2];
   double last_t_fluid = 0, last_t_solid = 0;
   std::string err;
 };
@@ -494,6 +503,7 @@ void hlbm_destroy(hlbm_ctx* ctx) {
   cudaFree(ctx->d_bits);
   cudaFree(ctx->d_fused);
   cudaFree(ctx->d_stage);
+  hlbm_ipc_close(ctx);
   free_mesh(ctx);
   for (int i = 0; i < 3; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -545,6 +555,83 @@ int hlbm_next_halo_planes(hlbm_ctx* ctx, void** send_lo, void** send_hi, void** 
   if (recv_lo) *recv_lo = b;
   if (recv_hi) *recv_hi = b + (int64_t)(ctx->cfg.nx + 1) * pb;
   if (bytes) *bytes = pb;
+  return HLBM_OK;
+}
+
+int hlbm_ipc_export(hlbm_ctx* ctx, void* handles, int32_t* cur) {
+  if (!ctx || !handles) return fail(ctx, HLBM_EINVAL, "null argument");
+  SETTLE(ctx);
+  for (int b = 0; b < 2; ++b)
+    CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handles) + b, ctx->buf[b]));
+  if (cur) *cur = ctx->cur;
+  return HLBM_OK;
+}
+
+int hlbm_ipc_open(hlbm_ctx* ctx, int32_t side, const void* handles, int32_t peer_nx, int32_t peer_cur) {
+  if (!ctx || !handles || side < 0 || side > 1 || peer_nx < 1 || (peer_cur & ~1))
+    return fail(ctx, HLBM_EINVAL, "bad arguments");
+  auto& P = ctx->peer[side];
+  if (P.open) return fail(ctx, HLBM_EINVAL, "neighbour already mapped (hlbm_ipc_close first)");
+  const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  const auto& O = ctx->peer[1 - side];
+  if (O.open && !memcmp(O.h, h, sizeof(O.h))) {   // the same rank on both sides (2 ranks, periodic)
+    P.buf[0] = O.buf[0];
+    P.buf[1] = O.buf[1];
+    P.owner = false;
+  } else {
+    for (int b = 0; b < 2; ++b) {
+      cudaError_t e = cudaIpcOpenMemHandle(&P.buf[b], h[b], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        if (b) cudaIpcCloseMemHandle(P.buf[0]);
+        P.buf[0] = P.buf[1] = nullptr;
+        return fail(ctx, HLBM_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+    }
+    P.owner = true;
+  }
+  memcpy(P.h, h, sizeof(P.h));
+  P.nx = peer_nx;
+  P.rel = (peer_cur ^ ctx->cur) & 1;
+  P.open = true;
+  return HLBM_OK;
+}
+
+int hlbm_ipc_sync(hlbm_ctx* ctx, int32_t side, int32_t peer_cur) {
+  if (!ctx || side < 0 || side > 1 || (peer_cur & ~1)) return fail(ctx, HLBM_EINVAL, "bad arguments");
+  if (!ctx->peer[side].open) return fail(ctx, HLBM_EINVAL, "neighbour not mapped");
+  SETTLE(ctx);
+  ctx->peer[side].rel = (peer_cur ^ ctx->cur) & 1;
+  return HLBM_OK;
+}
+
+int hlbm_halo_push(hlbm_ctx* ctx, int32_t next_buffer, void* stream) {
+  if (!ctx) return HLBM_EINVAL;
+  if (!next_buffer) SETTLE(ctx);
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  const int64_t pb = ctx->plane_elems * 4;
+  const int mine = next_buffer ? 1 - ctx->cur : ctx->cur;
+  const char* b = (const char*)ctx->buf[mine];
+  for (int side = 0; side < 2; ++side) {
+    const auto& P = ctx->peer[side];
+    if (!P.open) continue;
+    char* dst = (char*)P.buf[mine ^ P.rel];
+    if (side == 0)   // our first interior plane -> the x-lo neighbour's hi ghost plane
+      CK(cudaMemcpyAsync(dst + (int64_t)(P.nx + 1) * pb, b + pb, pb, cudaMemcpyDeviceToDevice, st));
+    else             // our last interior plane -> the x-hi neighbour's lo ghost plane
+      CK(cudaMemcpyAsync(dst, b + (int64_t)ctx->cfg.nx * pb, pb, cudaMemcpyDeviceToDevice, st));
+  }
+  return HLBM_OK;
+}
+
+int hlbm_ipc_close(hlbm_ctx* ctx) {
+  if (!ctx) return HLBM_EINVAL;
+  if (!ctx->peer[0].open && !ctx->peer[1].open) return HLBM_OK;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& P : ctx->peer) {
+    if (P.open && P.owner)
+      for (int b = 0; b < 2; ++b) cudaIpcCloseMemHandle(P.buf[b]);
+    P = hlbm_ctx::Peer{};
+  }
   return HLBM_OK;
 }
 

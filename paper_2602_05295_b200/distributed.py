@@ -13,6 +13,18 @@ device, in stream order on the compute stream.  Ranks at a non-periodic x face h
 ghost plane is resolved by the BC inside the kernels (inflow constants / outflow clamp /
 wall bounce-back).
 
+Transports: ``transport="p2p"`` (default) posts the planes as ``torch.distributed`` send/recv
+pairs; ``transport="ipc"`` is the peer-store halo of SURVEY.md §8e (K6): every rank maps its
+neighbours' state buffers once through CUDA IPC (``Solver.ipc_export`` / ``ipc_open``;
+NVLink peer memory when the neighbours sit on other GPUs) and copies its freshly written edge
+planes straight into their ghost planes (``Solver.halo_push``, a device-to-device copy on the
+comm stream).  Ordering across processes uses interprocess CUDA events, two per kind
+alternating by step parity: before writing into a neighbour's ghost plane a rank's comm stream
+waits for that neighbour's edge kernels of the previous step (the last readers of that plane),
+and a rank's edge kernels wait for the neighbours' pushes of the previous step.  A stream can
+only wait for an event record that the other process has already issued, so each step starts
+with a host barrier on a gloo group (no device synchronisation; the host runs ahead of the GPU).
+
 Overlap: a step computes its two edge destination planes
 (``step_range(0, 1)``, ``step_range(nx-1, nx)``) on a side stream while the bulk
 ``step_range(1, nx-1)`` runs on the compute stream; the exchange of the edge planes into the
@@ -115,7 +127,7 @@ class DistributedSolver:
 
     def __init__(self, global_dims: Sequence[int], config, mask: Optional[np.ndarray] = None,
                  rank: Optional[int] = None, world: Optional[int] = None, group=None, solver=None,
-                 overlap: bool = True):
+                 overlap: bool = True, transport: str = "p2p"):
         import torch
         import torch.distributed as dist
 
@@ -149,6 +161,11 @@ class DistributedSolver:
             self._comm_stream = torch.cuda.Stream()
             self._edge_stream = torch.cuda.Stream()   # edge planes, concurrent with the bulk
         self._synced_version = None   # solver state version whose ghost planes are exchanged
+        if transport not in ("p2p", "ipc"):
+            raise ValueError("transport must be 'p2p' or 'ipc'")
+        self.transport = transport
+        if transport == "ipc":
+            self._setup_ipc()
 
     # ------------------------------------------------------------------ exchange
     def _halo_tensors(self, next_buffer: bool):
@@ -197,11 +214,105 @@ class DistributedSolver:
             self._torch.cuda.current_stream().wait_event(self._comm_done)
             self._comm_done = None
 
+    # ------------------------------------------------------------------ peer-store halo (ipc)
+    def _neighbours(self):
+        return sorted({r for r in (self.plan.lo, self.plan.hi) if r is not None})
+
+    def _setup_ipc(self):
+        import torch
+        import torch.distributed as dist
+        if not self._cuda or not hasattr(self.solver, "ipc_export"):
+            raise ValueError("transport='ipc' needs the CUDA Solver")
+        if not self.overlap or self.plan.nx <= 2:
+            raise ValueError("transport='ipc' needs the overlapped schedule and > 2 planes per rank")
+        # host ordering of the interprocess event records (see the module docstring)
+        self._hostpg = self.group if dist.get_backend(self.group) == "gloo" else dist.new_group(backend="gloo")
+        self._ev_edge = [torch.cuda.Event(interprocess=True) for _ in range(2)]
+        self._ev_push = [torch.cuda.Event(interprocess=True) for _ in range(2)]
+        handles, cur = self.solver.ipc_export()
+        info = {"nx": self.plan.nx, "handles": handles, "cur": cur,
+                "edge": [e.ipc_handle() for e in self._ev_edge], "push": [e.ipc_handle() for e in self._ev_push]}
+        allinfo = [None] * self.world
+        dist.all_gather_object(allinfo, info, group=self._hostpg)
+        dev = torch.cuda.current_device()
+        self._peer_ev = {}
+        for r in self._neighbours():
+            self._peer_ev[r] = ([torch.cuda.Event.from_ipc_handle(dev, h) for h in allinfo[r]["edge"]],
+                                [torch.cuda.Event.from_ipc_handle(dev, h) for h in allinfo[r]["push"]])
+        for side, r in ((0, self.plan.lo), (1, self.plan.hi)):
+            if r is not None:
+                self.solver.ipc_open(side, allinfo[r]["handles"], allinfo[r]["nx"], allinfo[r]["cur"])
+        self._k = 0   # steps since the last prime (event parity)
+
+    def _prime_ipc(self):
+        """Collective: re-align the neighbours' buffer indices and push the current edge planes."""
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        _, cur = self.solver.ipc_export()
+        curs = [None] * self.world
+        dist.all_gather_object(curs, cur, group=self._hostpg)   # also the barrier before the push
+        for side, r in ((0, self.plan.lo), (1, self.plan.hi)):
+            if r is not None:
+                self.solver.ipc_sync(side, curs[r])
+        self.solver.halo_push(False, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        dist.barrier(group=self._hostpg)
+        self._k = 0
+        self._synced_version = self._state_version()
+
+    def _one_step_ipc(self, with_stats: bool):
+        import torch
+        import torch.distributed as dist
+        s, nx = self.solver, self.plan.nx
+        # the step-start barrier also decides collectively whether a prime is due
+        flag = torch.tensor([1.0 if self._synced_version != self._state_version() else 0.0])
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self._hostpg)
+        if flag.item() > 0:
+            self._prime_ipc()
+        p = self._k & 1
+        compute = torch.cuda.current_stream()
+        compute.wait_event(self._ev_push[p])     # our push of step k-2 read the planes step k writes
+        s.step_begin(with_stats)
+        start = torch.cuda.Event()
+        start.record(compute)
+        es, cs = self._edge_stream, self._comm_stream
+        es.wait_event(start)
+        if self._k > 0:
+            for r in self._neighbours():        # their step k-1 planes are in our ghost planes
+                es.wait_event(self._peer_ev[r][1][p ^ 1])
+        s.step_range(0, 1, es.cuda_stream)
+        s.step_range(nx - 1, nx, es.cuda_stream)
+        self._ev_edge[p].record(es)
+        cs.wait_event(self._ev_edge[p])
+        if self._k > 0:
+            for r in self._neighbours():        # their step k-1 edges were the last readers of the
+                cs.wait_event(self._peer_ev[r][0][p ^ 1])   # ghost planes we overwrite
+        s.halo_push(True, cs.cuda_stream)
+        self._ev_push[p].record(cs)
+        s.step_range(1, nx - 1)
+        compute.wait_event(self._ev_edge[p])
+        s.step_end()
+        self._k += 1
+        self._synced_version = self._state_version()
+
+    def close(self):
+        """Unmap the neighbours (ipc) after every rank's work is done (collective)."""
+        if self.transport == "ipc" and self._cuda:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.synchronize()
+            dist.barrier(group=self._hostpg)      # no rank still pushes into our buffers
+            self.solver.ipc_close()
+            dist.barrier(group=self._hostpg)      # every mapping closed before any buffer is freed
+
     # ------------------------------------------------------------------ stepping
     def _state_version(self):
         return getattr(self.solver, "state_version", 0)
 
     def _one_step(self, with_stats: bool):
+        if self.transport == "ipc":
+            return self._one_step_ipc(with_stats)
         s = self.solver
         nx = self.plan.nx
         if self._synced_version != self._state_version():

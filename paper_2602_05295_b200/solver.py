@@ -465,6 +465,33 @@ class Solver:
         self._chk(fn(self._ctx, *(C.byref(x) for x in p), C.byref(nb)))
         return [x.value for x in p], nb.value
 
+    # peer-store halo through CUDA IPC (include/hlbm.h hlbm_ipc_*; DistributedSolver transport="ipc")
+    def ipc_export(self):
+        """(handles: 128 bytes, current buffer index) for the neighbours' ``ipc_open``."""
+        buf = C.create_string_buffer(128)
+        cur = C.c_int32()
+        self._chk(self._lib.hlbm_ipc_export(self._ctx, buf, C.byref(cur)))
+        return buf.raw, cur.value
+
+    def ipc_open(self, side: int, handles: bytes, peer_nx: int, peer_cur: int):
+        if len(handles) != 128:
+            raise ValueError("expected the 128 bytes of ipc_export")
+        buf = C.create_string_buffer(handles, 128)
+        self._chk(self._lib.hlbm_ipc_open(self._ctx, int(side), buf, int(peer_nx), int(peer_cur)))
+
+    def ipc_sync(self, side: int, peer_cur: int):
+        self._chk(self._lib.hlbm_ipc_sync(self._ctx, int(side), int(peer_cur)))
+
+    def current_buffer(self) -> int:
+        return self.ipc_export()[1]
+
+    def halo_push(self, next_buffer: bool, stream_ptr: Optional[int] = None):
+        self._chk(self._lib.hlbm_halo_push(self._ctx, int(bool(next_buffer)),
+                                           C.c_void_p(int(stream_ptr)) if stream_ptr else None))
+
+    def ipc_close(self):
+        self._chk(self._lib.hlbm_ipc_close(self._ctx))
+
     # one step split into x-ranges of destination planes (overlapped multi-GPU schedule)
     def step_begin(self, with_stats: bool = False):
         self._chk(self._lib.hlbm_step_begin(self._ctx, int(with_stats)))

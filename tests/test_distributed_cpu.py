@@ -187,3 +187,15 @@ def test_overlapped_schedule_reproduces_single_domain(world, bc_x, overlap):
         nx = st.shape[1]
         assert ranges == ([(0, 1), (nx - 1, nx), (1, nx - 1)] if overlap else [(0, nx)] * 3)
     np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14)
+
+
+def test_transport_validation():
+    """transport="ipc" needs the CUDA Solver (it maps the neighbours' device buffers); unknown
+    transports are rejected."""
+    from paper_2602_05295_b200 import SolverConfig
+    from paper_2602_05295_b200.distributed import DistributedSolver
+    cfg = SolverConfig(nu=0.02)
+    with pytest.raises(ValueError, match="ipc"):
+        DistributedSolver((8, 4, 4), cfg, rank=0, world=1, solver=object(), transport="ipc")
+    with pytest.raises(ValueError, match="transport"):
+        DistributedSolver((8, 4, 4), cfg, rank=0, world=1, solver=object(), transport="tcp")

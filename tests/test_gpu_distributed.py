@@ -45,7 +45,7 @@ def _inputs(kind):
     return state, mask
 
 
-def _worker(rank, world, port, kind, steps, out):
+def _worker(rank, world, port, kind, steps, out, transport="p2p"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
@@ -56,13 +56,24 @@ def _worker(rank, world, port, kind, steps, out):
         torch.cuda.set_device(0)
         cfg = _config(kind)
         state, mask = _inputs(kind)
-        ds = DistributedSolver(GDIMS, cfg, mask=mask)
+        ds = DistributedSolver(GDIMS, cfg, mask=mask, transport=transport)
         p = ds.plan
         sl = slice(p.x0, p.x0 + p.nx)
         ds.solver.set_moments(state[0][sl], state[1][:, sl], state[2][:, sl])
-        st = ds.step(steps)
+        if transport == "ipc" and rank == 0:
+            # set_moments swaps the rank's buffers: rank 0's current index now differs from the
+            # one its neighbours mapped at construction -- the prime must re-align them
+            ds.solver.set_moments(state[0][sl], state[1][:, sl], state[2][:, sl])
+        if transport == "ipc":
+            # a host-side state change mid-run (set_moments swaps the rank's buffers) re-primes
+            ds.step(steps // 2, stats=False)
+            ds.solver.set_state(ds.solver.get_state())
+            st = ds.step(steps - steps // 2)
+        else:
+            st = ds.step(steps)
         res = ds.solver.get_state()
         out[rank] = (p.x0, res, st.mass, int(st.n_fluid))
+        ds.close()
         ds.solver.close()
     finally:
         dist.destroy_process_group()
@@ -94,6 +105,26 @@ def test_distributed_solver_real_slabs_bitwise(world, kind):
         assert nf == st.n_fluid
     assert np.array_equal(got, ref)
     assert mass == pytest.approx(st.mass, rel=1e-9)
+
+
+@pytest.mark.parametrize("world,kind", [(2, "periodic_q16"), (3, "periodic_q16"), (3, "channel_q16"),
+                                        (2, "channel_fp32")])
+def test_distributed_solver_ipc_peer_store_bitwise(world, kind):
+    """transport="ipc": CUDA IPC mappings of the neighbours' buffers, edge planes pushed straight
+    into their ghost planes, interprocess events between the ranks' streams."""
+    steps = 7
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, kind, steps, out, "ipc"), nprocs=world, join=True)
+    ref, st = _single(kind, steps)
+    got = np.zeros_like(ref)
+    for r in range(world):
+        x0, res, m, nf = out[r]
+        got[:, x0:x0 + res.shape[1]] = res
+        assert nf == st.n_fluid
+    assert np.array_equal(got, ref)
+    assert m == pytest.approx(st.mass, rel=1e-9)
 
 
 def _diverge_worker(rank, world, port, out):
