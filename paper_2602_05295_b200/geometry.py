@@ -228,3 +228,48 @@ def save_obj(path, vertices, faces):
             f.write(f"v {float(v[0])!r} {float(v[1])!r} {float(v[2])!r}\n")
         for a, b, c in np.asarray(faces, dtype=np.int64):
             f.write(f"f {a + 1} {b + 1} {c + 1}\n")
+
+
+def icosphere(center, radius, subdiv=1):
+    """Closed triangle mesh of a sphere: the icosahedron's 12 vertices / 20 faces, each face split
+    into 4 `subdiv` times with the new vertices pushed onto the sphere (scene geometry for the
+    triangle-mesh path; 20 * 4^subdiv faces)."""
+    g = (1.0 + 5 ** 0.5) / 2.0
+    V = [np.array(v, dtype=np.float64) for v in
+         ((-1, g, 0), (1, g, 0), (-1, -g, 0), (1, -g, 0), (0, -1, g), (0, 1, g), (0, -1, -g), (0, 1, -g),
+          (g, 0, -1), (g, 0, 1), (-g, 0, -1), (-g, 0, 1))]
+    V = [v / np.linalg.norm(v) for v in V]
+    F = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2),
+         (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5),
+         (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(subdiv):
+        mids = {}
+
+        def midpoint(a, b):
+            e = (a, b) if a < b else (b, a)
+            if e not in mids:
+                m = V[a] + V[b]
+                V.append(m / np.linalg.norm(m))
+                mids[e] = len(V) - 1
+            return mids[e]
+        nf = []
+        for a, b, c in F:
+            ab, bc, ca = midpoint(a, b), midpoint(b, c), midpoint(c, a)
+            nf += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        F = nf
+    return np.array(V) * float(radius) + np.asarray(center, dtype=np.float64), np.array(F, dtype=np.int64)
+
+
+def taylor_green_fields(n, u0=0.05):
+    """Taylor-Green vortex on an n^3 periodic box: (rho, u) for
+    ``Solver.set_equilibrium`` -- u = u0 (sin x cos y cos z, -cos x sin y cos z, 0), k = 2 pi / n,
+    with the matching pressure field in rho."""
+    k = 2 * np.pi / n
+    x = np.arange(n)[:, None, None]
+    y = np.arange(n)[None, :, None]
+    z = np.arange(n)[None, None, :]
+    u = np.zeros((3, n, n, n))
+    u[0] = u0 * np.sin(k * x) * np.cos(k * y) * np.cos(k * z)
+    u[1] = -u0 * np.cos(k * x) * np.sin(k * y) * np.cos(k * z)
+    rho = 1.0 + 3.0 * (u0 ** 2 / 16.0) * (np.cos(2 * k * x) + np.cos(2 * k * y)) * (np.cos(2 * k * z) + 2.0)
+    return np.broadcast_to(rho, (n, n, n)).copy(), u

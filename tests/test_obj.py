@@ -42,3 +42,16 @@ def test_malformed_records(tmp_path, body, msg):
     p.write_text(body)
     with pytest.raises(ValueError, match=msg):
         load_obj(p)
+
+
+def test_scene_helpers_match_the_oracle_inputs():
+    """geometry.icosphere / taylor_green_fields (the tools' scene inputs) equal the oracle's."""
+    from oracle import mesh as M
+    from oracle import step as OS
+    from paper_2602_05295_b200.geometry import icosphere, taylor_green_fields
+    V, F = icosphere((3.0, 4.0, 5.0), 2.5, 2)
+    V0, F0 = M.icosphere((3.0, 4.0, 5.0), 2.5, 2)
+    assert np.array_equal(F, F0) and np.allclose(V, V0, rtol=0, atol=1e-13)
+    rho, u = taylor_green_fields(16)
+    r0, m0, _ = OS.taylor_green(16)
+    assert np.allclose(rho, r0, rtol=0, atol=1e-15) and np.allclose(rho * u, m0, rtol=0, atol=1e-15)

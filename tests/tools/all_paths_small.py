@@ -3,7 +3,7 @@ tiny grids -- interior (fp32, q16 + dither + stats + solids), compacted lists (v
 the stream operator, per-cell step, import / export, D3Q19."""
 import sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import numpy as np
 from oracle import mesh as M
 from oracle import step as OS

@@ -1,7 +1,7 @@
 """Ad-hoc GPU bring-up checks (development tool; the pytest suite holds the real tests)."""
 import sys, time
 from pathlib import Path
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 import numpy as np
 from oracle import codec, step as ostep

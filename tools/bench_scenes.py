@@ -19,7 +19,6 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 
-from oracle.step import taylor_green
 from paper_2602_05295_b200 import QuantSpec, SimGrid, Solver, SolverConfig
 from paper_2602_05295_b200.geometry import sphere_mask, turbulence_modes, vehicle_mask, voxel_surface_mesh
 
@@ -65,8 +64,9 @@ def run(name, dims, cfg, init, mask=None, steps=50, mesh=None):
 
 
 def main():
-    tgv = taylor_green(64)
-    run("1 TGV 64^3", (64, 64, 64), SolverConfig(nu=0.01), lambda s: s.set_moments(*tgv), steps=200)
+    from paper_2602_05295_b200.geometry import taylor_green_fields
+    tgv = taylor_green_fields(64)
+    run("1 TGV 64^3", (64, 64, 64), SolverConfig(nu=0.01), lambda s: s.set_equilibrium(*tgv), steps=200)
     for prec in ("fp32", "q16"):
         run("2 turbulence box", (512, 512, 512), SolverConfig(nu=1e-4, precision=prec),
             lambda s: s.init_modes(turbulence_modes(512)))
@@ -82,7 +82,7 @@ def main():
     for prec in ("fp32", "q16"):
         run("3 sphere channel", dims, SolverConfig(nu=1e-4, bc=bc, u_in=(0.1, 0, 0), precision=prec),
             uniform(0.1), mask=m)
-    from oracle.mesh import icosphere
+    from paper_2602_05295_b200.geometry import icosphere
     sph = icosphere((128, 128, 128), 32.0, 5)
     run("3b sphere channel, triangle mesh", dims, SolverConfig(nu=1e-4, bc=bc, u_in=(0.1, 0, 0), precision="q16"),
         uniform(0.1), mesh=sph)

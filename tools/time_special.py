@@ -6,11 +6,10 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
-from oracle import mesh as M
 from paper_2602_05295_b200 import SimGrid, Solver, SolverConfig
 dims = (512, 256, 256)
 cfg = SolverConfig(nu=1e-3, precision="q16", bc={"x": ("inflow", "outflow")}, u_in=(0.05, 0, 0))
-from paper_2602_05295_b200.geometry import sphere_mask
+from paper_2602_05295_b200.geometry import icosphere, sphere_mask
 one = np.zeros(dims, np.uint8)
 one[400, 10, 10] = 1
 for sub in (None, 3, "voxel", "one"):
@@ -20,7 +19,7 @@ for sub in (None, 3, "voxel", "one"):
         elif sub == "one":
             s.set_mask(one)
         elif sub is not None:
-            V, F = M.icosphere((128.3, 127.7, 128.1), 32.0, sub)
+            V, F = icosphere((128.3, 127.7, 128.1), 32.0, sub)
             s.set_mesh(V, F)
         s.set_stream(torch.cuda.current_stream().cuda_stream)
         s.init_modes(np.array([[0, 0, 0, 0.05, 0, 0, np.pi / 2]]))
