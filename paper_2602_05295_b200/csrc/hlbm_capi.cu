@@ -433,6 +433,8 @@ int hlbm_create(const hlbm_config* cfg, hlbm_ctx** out) {
     const double sc = L / (mx - mn);
     ctx->Q.enc_scale[k] = (float)sc;
     ctx->Q.enc_off[k] = (float)((shift - mn) * sc + 0.5);
+    ctx->Q.enc_int[k] = (float)std::floor((shift - mn) * sc + 0.5);
+    ctx->Q.enc_frac[k] = (float)((shift - mn) * sc + 0.5 - std::floor((shift - mn) * sc + 0.5));
     ctx->Q.enc_nb[k] = (float)(-1.5 + 1.0 / 131072.0 - ((double)ctx->Q.enc_off[k] - ((shift - mn) * sc + 0.5)));
     const double mid = 0.5 * (mn + mx), half = 0.5 * (mx - mn);
     ctx->Q.sat_a[k] = (float)(1.0 / half);

@@ -161,8 +161,10 @@ __device__ __forceinline__ void store_cell(const StepArgs& A, int x, int y, int 
     uint32_t code[10];
 #pragma unroll
     for (int c = 0; c < 10; ++c) {
-      float t = __fmaf_rn(s[c], A.Q.enc_scale[c], A.Q.enc_off[c]);
-      if (DITHER) t = __fadd_rd(t, nz[c]);   // hlbm_math.cuh noise16u
+      // floor(t) = the floor of the exact value (hlbm_math.cuh Codec::enc_int, noise16u)
+      float t = DITHER ? __fadd_rd(__fmaf_rn(s[c], A.Q.enc_scale[c], A.Q.enc_off[c]), nz[c])
+                : A.Q.enc_frac[c] == 0.f ? __fmaf_rd(s[c], A.Q.enc_scale[c], A.Q.enc_int[c])
+                                         : __fadd_rd(__fmaf_rn(s[c], A.Q.enc_scale[c], A.Q.enc_frac[c]), A.Q.enc_int[c]);
       code[c] = min(f2u16_floor(t), A.Q.levels[c]);
       const float r = __fmaf_rn(s[c], A.Q.sat_a[c], A.Q.sat_b[c]);
       if (stat && !(fabsf(r) <= 1.0f)) atomicAdd(&A.stats->sat[c], 1ull);

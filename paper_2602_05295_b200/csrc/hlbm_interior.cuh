@@ -355,6 +355,10 @@ struct DefQ {
     return ((c == 0 ? 1.0 : 0.0) - mn(c)) * (65535.0 / (mx(c) - mn(c))) + 0.5;
   }
   __host__ __device__ static constexpr float enc_off(int c) { return (float)enc_off_d(c); }
+  __host__ __device__ static constexpr float enc_int(int c) { return (float)(double)(long long)enc_off_d(c); }
+  __host__ __device__ static constexpr float enc_frac(int c) {
+    return (float)(enc_off_d(c) - (double)(long long)enc_off_d(c));
+  }
   __host__ __device__ static constexpr float enc_nb(int c) {   // Codec::enc_nb
     return (float)(-1.5 + 1.0 / 131072.0 - ((double)enc_off(c) - enc_off_d(c)));
   }
@@ -376,6 +380,20 @@ template <int QMODE> __device__ __forceinline__ float q_enc_scale(const Codec& Q
 }
 template <int QMODE> __device__ __forceinline__ float q_enc_off(const Codec& Q, int c) {
   return QMODE == 2 ? DefQ::enc_off(c) : Q.enc_off[c];
+}
+// t = m * scale + enc_off ready for floor(): round-to-nearest when a dither add (rounding down)
+// follows; else rounded down -- in one FMA when enc_off is an integer, else as (m * scale + frac)
+// + int (Codec::enc_int).  The same rule as store_cell (hlbm_cells.cuh).
+template <bool DITHER, int QMODE>
+__device__ __forceinline__ V q_encode_t(const Codec& Q, int c, V m) {
+  const V sc = vsplat(q_enc_scale<QMODE>(Q, c));
+  if (DITHER) return vfma(m, sc, vsplat(q_enc_off<QMODE>(Q, c)));
+  if (QMODE == 2) {
+    if (DefQ::enc_frac(c) == 0.f) return vfma_rd(m, sc, vsplat(DefQ::enc_int(c)));
+    return vadd_rd(vfma(m, sc, vsplat(DefQ::enc_frac(c))), vsplat(DefQ::enc_int(c)));
+  }
+  return Q.enc_frac[c] == 0.f ? vfma_rd(m, sc, vsplat(Q.enc_int[c]))
+                              : vadd_rd(vfma(m, sc, vsplat(Q.enc_frac[c])), vsplat(Q.enc_int[c]));
 }
 
 // PRE: the values come out in the coeffs_pre input scales (hlbm_math.cuh) -- folded into the
@@ -519,7 +537,7 @@ __device__ __forceinline__ void store_pair(const StepArgs& A, const V m[10], int
     V t[10];
 #pragma unroll
     for (int c = 0; c < 10; ++c)
-      t[c] = vfma(s[c], vsplat(q_enc_scale<QMODE>(A.Q, c)), vsplat(q_enc_off<QMODE>(A.Q, c)));
+      t[c] = q_encode_t<DITHER, QMODE>(A.Q, c, s[c]);
     if (STATS) {
       // saturation counters: m outside [min, max]  (checked before the dither is added)
       bool satx, saty;

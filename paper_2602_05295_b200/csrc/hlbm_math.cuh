@@ -25,6 +25,7 @@ typedef float2 V;
 __device__ __forceinline__ V vsplat(float s) { return make_float2(s, s); }
 __device__ __forceinline__ V vadd(V a, V b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ V vadd_rd(V a, V b) { return __fadd2_rd(a, b); }
+__device__ __forceinline__ V vfma_rd(V a, V b, V c) { return __ffma2_rd(a, b, c); }
 __device__ __forceinline__ V vsub(V a, V b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 __device__ __forceinline__ V vmul(V a, V b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ V vmul(V a, float s) { return __fmul2_rn(a, vsplat(s)); }
@@ -315,6 +316,11 @@ struct Codec {
                         // a linear mass / momentum drift over long dithered runs)
   float enc_scale[10];  // (2^b-1)/(max-min)
   float enc_off[10];    // -min*scale + 1/2   (component 0: -(min-1)*scale + 1/2)
+  float enc_int[10];    // enc_off split into an integer and a fraction: without dither the
+  float enc_frac[10];   // encode is t = (m*scale + frac) + int, the second add rounding down, so
+                        // floor(t) is the floor of the exact value (a round-to-nearest t at ~2^15,
+                        // ulp 2^-9..2^-8, would lift values just below an integer onto it, and
+                        // enc_off itself is not exact in fp32 for rho: -5.6e-4 LSB)
   float enc_nb[10];     // dither offset: noise = u + enc_nb, u = 1 + bits/2^16 in [1, 2);
                         // -3/2 + 2^-17 (zero-mean noise) - (float(enc_off) - enc_off) (the
                         // offset's fp32 rounding), so that E[code] is the exact scaled value

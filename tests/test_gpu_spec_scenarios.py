@@ -115,7 +115,9 @@ def test_periodic_mass_momentum_conservation_1000_steps():
         s.set_moments(*state)
         m0 = s.step(1)
         m1 = s.step(999)
-    assert abs(m1.mass - m0.mass) / m0.mass < 1e-7          # fp32 state (SPEC's 1e-10 is for 64-bit)
+    # SPEC.md:490 asks < 1e-10 of its float64 reference; the fp32 state measures 1e-10 here
+    # (tools/mass_drift.py: -9.8e-11 at 32^3, -5.9e-11 at 128^3)
+    assert abs(m1.mass - m0.mass) / m0.mass < 1e-9
     np.testing.assert_allclose(m1.momentum, m0.momentum, atol=1e-6 * np.prod(shape) * 0.03)
 
 
@@ -131,3 +133,21 @@ def test_obj_mesh_drives_the_same_cut_links(tmp_path):
             res.append(s.cut_links())
     for a, b in zip(res[0], res[1]):
         assert np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dither", [True, False])
+def test_q16_mass_drift_1000_steps(dither):
+    """The 16-bit codec carries no systematic bias: re-centred decode, encode
+    rounded down before the floor (dither: the noise add; none: the split enc_off), so the mass of a
+    periodic box only random-walks.  The biased codec drifted 4.5e-6 in 1000 steps at 128^3 without
+    dither (+1.9e-4 in 20 000 steps at 512^3 with it); now 9e-8 / 1.1e-7."""
+    shape = (128, 128, 128)
+    rng = np.random.default_rng(3)
+    rho = 1.0 + rng.uniform(-0.02, 0.02, shape)
+    u = rng.uniform(-0.03, 0.03, (3,) + shape)
+    cfg = SolverConfig(nu=0.02, precision="q16", quant=QuantSpec(dither=dither), seed=1)
+    with Solver(SimGrid(shape), cfg) as s:
+        s.set_equilibrium(rho, u)
+        m0 = s.step(1)
+        m1 = s.step(999)
+    assert abs(m1.mass - m0.mass) / m0.mass < 1e-6
