@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
     Part6 Ma, Mb, Na, Nb;   // rotating plane partials (x2 unroll, see Part6)
 #pragma unroll
     for (int k = 0; k < 6; ++k) Ma.a[k] = Na.a[k] = Nb.a[k] = vsplat(0.f);
-    const int wu = w - 1, wd = (w + 1) & (kNW - 1);   // exchange rows read by this warp
+    const int wu = w - 1, wd = (w + 1) % kNW;   // exchange rows read by this warp
     const int64_t cell0 = (int64_t)(yrow + 1) * g.zp + (zc + kZOff);   // pair offset inside a plane
 
     // one source plane p: Mq, Nq (dest q = p-1), Np (dest p) carried in; nb = M of dest p and

@@ -24,7 +24,7 @@ namespace hlbm {
 #define HLBM_NW 16
 #endif
 constexpr int kNW = HLBM_NW;     // warps per CTA: halo warp(s) + one warp per interior y row
-constexpr int kCtaPerSm = 16 / kNW;   // resident CTAs per SM (128 registers per thread)
+constexpr int kCtaPerSm = kNW > 16 ? 1 : 16 / kNW;   // resident CTAs per SM (<= 128 registers per thread)
 constexpr int kHaloWarps = HLBM_HALO_WARPS;   // 1: warp 0 does both halo rows; 2: warps 0 and 15
 constexpr int kRows = kNW - kHaloWarps;   // interior rows per tile
 constexpr int kBoxRows = kRows + 2;   // rows of a plane tile in shared memory (+1 halo row per side)
