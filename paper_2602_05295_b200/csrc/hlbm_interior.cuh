@@ -729,6 +729,13 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
 #pragma unroll
     for (int k = 0; k < 6; ++k) Ma.a[k] = Na.a[k] = Nb.a[k] = vsplat(0.f);
     const int wu = w - 1, wd = (w + 1) % kNW;   // exchange rows read by this warp
+    // rows past the first row beyond ny (the last y tile of a grid whose ny is not a multiple of
+    // kRows) feed nothing that is stored: such a warp keeps the barrier protocol -- same waits and
+    // arrivals, so the ring's phases stay paced -- and skips the arithmetic, leaving its SM
+    // sub-partition's issue slots to the active rows (q16 no-stats: 512^3 1.764 -> 1.743 ms,
+    // 400^3 0.854 -> 0.840, 256^3 0.285 -> 0.280; the STATS variants came out ~1% slower with the
+    // second loop and the HBM-bound fp32 kernel gained nothing, so they keep the single loop)
+    const bool active = !HLBM_IDLE_ROWS || STATS || !Q16 || yrow <= g.ny;
     const int64_t cell0 = (int64_t)(yrow + 1) * g.zp + (zc + kZOff);   // pair offset inside a plane
 
     // one source plane p: Mq, Nq (dest q = p-1), Np (dest p) carried in; nb = M of dest p and
@@ -773,9 +780,26 @@ __global__ void __launch_bounds__(kNW * 32, kCtaPerSm) fluid_interior(const __gr
       }
     };
 
-    for (int it = 0; it < NP; it += 2) {
-      body(it, Ma, Nb, Na, Mb);
-      if (it + 1 < NP) body(it + 1, Mb, Na, Nb, Ma);
+    if (active) {
+      for (int it = 0; it < NP; it += 2) {
+        body(it, Ma, Nb, Na, Mb);
+        if (it + 1 < NP) body(it + 1, Mb, Na, Nb, Ma);
+      }
+    } else {
+      // the same waits and arrivals per plane as `body`, no arithmetic
+      for (int it = 0; it < NP; ++it) {
+        const int b = (NB == 2) ? (it & 1) : 0;
+        const uint32_t eph = (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u;
+        mbar_wait(&S.bar[st], sph);
+        consumed();
+        mbar_wait(&S.empty[b][w], eph ^ 1u);
+        if (++st == STAGES) { st = 0; sph ^= 1u; }
+        mbar_arrive(&S.full[b][w]);
+        mbar_wait(&S.full[b][wu], eph);
+        mbar_wait(&S.full[b][wd], eph);
+        mbar_arrive(&S.empty[b][wu]);
+        mbar_arrive(&S.empty[b][wd]);
+      }
     }
   }
 
