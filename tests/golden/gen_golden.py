@@ -13,6 +13,14 @@ outputs of the reference's own functions:
   tgv32.npz          Taylor-Green 32^3 after 10 steps, same composition
   d3q19.npz          make_lattice("D3Q19") tables and 1 / 3 periodic steps of a random
                      12x14x16 state with the D3Q19 lattice, same composition
+`--extra` (SURVEY.md §8c's remaining golden vectors; same composition, codec and lists
+written out here from SPEC, independent of oracle/):
+  q16_step16.npz     16-bit codes of a random 16^3 state (SPEC.md:345-353 quantizer, default
+                     QuantSpec, no dither) and of its state after one reference step
+  sphere32.npz       sphere mask in a periodic 32^3 box -> sorted boundary list + link masks
+                     (bit i: x - c_i solid, reference direction order) + solid list
+  tgv64.npz          Taylor-Green 64^3 (nu = 0.01): kinetic energy and mass after every step to
+                     200, and the planes x = 0 and x = 21 of the state after 1, 10 and 200 steps
 """
 
 from __future__ import annotations
@@ -117,8 +125,65 @@ def main():
     print("golden fixtures written to", HERE)
 
 
+QMIN = np.array([0.8, -0.6, -0.6, -0.6, -0.1, -0.1, -0.1, -0.1, -0.1, -0.1])
+QMAX = np.array([1.5, 0.6, 0.6, 0.6, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1])
+
+
+def quantize16(rho, mom, stress):
+    """SPEC.md:345-353: q = floor((clamp(m) - min) / (max - min) * (2^16 - 1) + 1/2), m = (rho,
+    rho u, sneq)."""
+    m = np.concatenate([rho[None], mom, RM.neq_decompose(rho, mom, stress)])
+    lo, hi = QMIN.reshape(-1, 1, 1, 1), QMAX.reshape(-1, 1, 1, 1)
+    x = (np.clip(m, lo, hi) - lo) / (hi - lo)
+    return np.clip(np.floor(x * 65535.0 + 0.5), 0, 65535).astype(np.uint16)
+
+
+def dequantize16(q):
+    lo, hi = QMIN.reshape(-1, 1, 1, 1), QMAX.reshape(-1, 1, 1, 1)
+    m = lo + q.astype(np.float64) * (hi - lo) / 65535.0
+    rho, mom = m[0], m[1:4]
+    return rho, mom, RM.neq_recompose(rho, mom, m[4:])
+
+
+def write_extra():
+    tau = 0.5 + 3 * 0.02
+    rho, mom, st = random_state((16, 16, 16), 5, 0.08, 0.08, 0.008)
+    q0 = quantize16(rho, mom, st)
+    q1 = quantize16(*ref_step(*dequantize16(q0), tau))
+    np.savez_compressed(HERE / "q16_step16.npz", tau=tau, codes0=q0, codes1=q1)
+
+    n = 32
+    g = np.indices((n, n, n)).astype(np.float64)
+    c = np.array([15.5, 16.2, 14.8]).reshape(3, 1, 1, 1)
+    mask = (((g - c) ** 2).sum(0) <= 7.3 ** 2).astype(np.uint8)
+    links = np.zeros((n, n, n), dtype=np.uint32)
+    for i, ci in enumerate(LAT.velocities):
+        if i:   # source x - c_i solid (periodic): np.roll(a, c)[x] = a[x - c]
+            links |= (np.roll(mask, shift=tuple(ci), axis=(0, 1, 2)).astype(np.uint32) << np.uint32(i))
+    fluid = mask == 0
+    bsel = fluid & (links != 0)
+    cells = np.flatnonzero(bsel.ravel()).astype(np.int64)
+    np.savez_compressed(HERE / "sphere32.npz", mask=mask, boundary_cells=cells,
+                        link_masks=links.ravel()[cells], solid_cells=np.flatnonzero(mask.ravel()).astype(np.int64))
+
+    tau = 0.5 + 3 * 0.01
+    r, m, s_ = taylor_green(64)
+    ke, mass, planes = [], [], {}
+    for k in range(1, 201):
+        r, m, s_ = ref_step(r, m, s_, tau)
+        ke.append(0.5 * float((m ** 2 / r).sum()))
+        mass.append(float(r.sum()))
+        if k in (1, 10, 200):
+            sn = RM.neq_decompose(r, m, s_)
+            planes[k] = np.concatenate([r[None], m, sn])[:, [0, 21]]
+    np.savez_compressed(HERE / "tgv64.npz", tau=tau, ke=np.array(ke), mass=np.array(mass),
+                        planes1=planes[1], planes10=planes[10], planes200=planes[200])
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["--d3q19"]:
         write_d3q19()
+    elif sys.argv[1:] == ["--extra"]:
+        write_extra()
     else:
         main()

@@ -91,3 +91,31 @@ def test_oracle_d3q19_matches_reference():
         np.testing.assert_allclose(g, r, rtol=0, atol=1e-15)
     for g, r in zip(got3, (z["rho3"], z["mom3"], z["stress3"])):
         np.testing.assert_allclose(g, r, rtol=0, atol=1e-14)
+
+
+# ---- SURVEY.md §8c's remaining golden vectors (gen_golden.py --extra: reference functions + SPEC
+# codec / list definitions written out in the generator, independent of oracle/)
+def test_oracle_q16_step_matches_reference_composition():
+    from oracle import codec
+    z = load("q16_step16.npz")
+    words = codec.pack(z["codes0"].astype(np.uint32))
+    got = codec.unpack(OS.fluid_step_q16(words, float(z["tau"]), 0)[0])
+    assert np.array_equal(got, z["codes1"].astype(np.uint32))   # float64 both sides: bit-exact
+
+
+def test_oracle_boundary_lists_match_reference_directions():
+    z = load("sphere32.npz")
+    cells, masks = OS.boundary_lists(z["mask"], OS.BC())
+    assert np.array_equal(cells, z["boundary_cells"])
+    assert np.array_equal(masks, z["link_masks"])
+    assert np.array_equal(OS.solid_cells(z["mask"]), z["solid_cells"])
+
+
+def test_oracle_tgv64_ten_steps():
+    z = load("tgv64.npz")
+    r, m, s = OS.taylor_green(64)
+    for _ in range(10):
+        r, m, s = OS.fluid_step(r, m, s, float(z["tau"]))
+    got = np.concatenate([r[None], m, OM.neq_decompose(r, m, s)])[:, [0, 21]]
+    np.testing.assert_allclose(got, z["planes10"], rtol=0, atol=1e-13)
+    assert 0.5 * float((m ** 2 / r).sum()) == __import__("pytest").approx(z["ke"][9], rel=1e-12)
