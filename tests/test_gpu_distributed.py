@@ -107,6 +107,48 @@ def test_distributed_solver_real_slabs_bitwise(world, kind):
     assert mass == pytest.approx(st.mass, rel=1e-9)
 
 
+def _jitter_worker(rank, world, port, steps, out):
+    """transport="ipc" with per-rank host delays between steps: ranks issue their steps out of
+    phase, so a rank's stream waits on neighbour events recorded at different host times."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import time
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_05295_b200.distributed import DistributedSolver
+        torch.cuda.set_device(0)
+        state, _ = _inputs("periodic_q16")
+        ds = DistributedSolver(GDIMS, _config("periodic_q16"), transport="ipc")
+        p = ds.plan
+        sl = slice(p.x0, p.x0 + p.nx)
+        ds.solver.set_moments(state[0][sl], state[1][:, sl], state[2][:, sl])
+        rng = np.random.default_rng(rank)
+        for _ in range(steps):
+            time.sleep(float(rng.uniform(0, 0.004)))
+            ds.step(1, stats=False)
+        out[rank] = (p.x0, ds.solver.get_state())
+        ds.close()
+        ds.solver.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_peer_store_with_host_jitter():
+    steps = 24
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_jitter_worker, args=(3, port, steps, out), nprocs=3, join=True)
+    ref, _ = _single("periodic_q16", steps)
+    got = np.zeros_like(ref)
+    for r in range(3):
+        x0, res = out[r]
+        got[:, x0:x0 + res.shape[1]] = res
+    assert np.array_equal(got, ref)
+
+
 @pytest.mark.parametrize("world,kind", [(2, "periodic_q16"), (3, "periodic_q16"), (3, "channel_q16"),
                                         (2, "channel_fp32")])
 def test_distributed_solver_ipc_peer_store_bitwise(world, kind):
