@@ -305,6 +305,7 @@ class DistributedSolver:
             dist.barrier(group=self._hostpg)      # no rank still pushes into our buffers
             self.solver.ipc_close()
             dist.barrier(group=self._hostpg)      # every mapping closed before any buffer is freed
+            self.transport = "closed"
 
     # ------------------------------------------------------------------ stepping
     def _state_version(self):
@@ -313,6 +314,8 @@ class DistributedSolver:
     def _one_step(self, with_stats: bool):
         if self.transport == "ipc":
             return self._one_step_ipc(with_stats)
+        if self.transport == "closed":
+            raise RuntimeError("DistributedSolver.step after close() (the neighbours are unmapped)")
         s = self.solver
         nx = self.plan.nx
         if self._synced_version != self._state_version():
