@@ -289,6 +289,53 @@ struct PullGroup<Q, CXW, Q16, FORCE, MODE, Q> {
   __device__ __forceinline__ static void run(const StepArgs&, int, int, int, uint32_t, float*, MeshCtx&) {}
 };
 
+// runtime-direction forms of eval_eo / pull_link (MODE 0): the same operations in the same order as
+// the templates (a skipped term is an added zero, a sign a negated operand), so bit-identical; one
+// link's code serves all 27, so a warp's 9 links fit the instruction cache (the fully unrolled
+// per-warp groups spent most of their stall samples on instruction fetch)
+template <int Q>
+__device__ __forceinline__ void eval_eo_rt(const Coef<float>& C, int cx, int cy, int cz, float& E, float& O) {
+  float e = C.K0;
+  if (cx) e = e + C.Qxx;
+  if (cy) e = e + C.Qyy;
+  if (cz) e = e + C.Qzz;
+  if (cx && cy) e = (cx * cy > 0) ? e + C.Qxy : e - C.Qxy;
+  if (cx && cz) e = (cx * cz > 0) ? e + C.Qxz : e - C.Qxz;
+  if (cy && cz) e = (cy * cz > 0) ? e + C.Qyz : e - C.Qyz;
+  float o = 0.f;
+  bool first = true;
+  auto acc = [&](int sgn, float v) {
+    if (first) { o = (sgn > 0) ? v : -v; first = false; }
+    else o = (sgn > 0) ? o + v : o - v;
+  };
+  if (cx) acc(cx, C.Lx);
+  if (cy) acc(cy, C.Ly);
+  if (cz) acc(cz, C.Lz);
+  if (cx && cy) { acc(cy, C.Txxy); acc(cx, C.Txyy); }
+  if (cx && cz) { acc(cz, C.Txxz); acc(cx, C.Txzz); }
+  if (cy && cz) { acc(cy, C.Tyzz); acc(cz, C.Tyyz); }
+  if (cx && cy && cz) acc(cx * cy * cz, C.Txyz);
+  const int c2 = cx * cx + cy * cy + cz * cz;
+  const float om = Q == 19 ? (c2 == 0 ? 72.f : (c2 == 1 ? 12.f : 6.f))
+                           : (cx ? 1.f : 4.f) * (cy ? 1.f : 4.f) * (cz ? 1.f : 4.f);
+  if (om != 1.f) { e = e * om; o = first ? o : o * om; }
+  E = e;
+  O = o;
+}
+
+template <bool Q16, bool FORCE, int Q>
+__device__ __forceinline__ void pull_link_rt(const StepArgs& A, int I, int x, int y, int z, uint32_t mask,
+                                             float m[10]) {
+  const int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
+  const bool bb = (mask >> I) & 1u;   // MODE 0: half-way bounce-back
+  float s[10];
+  load_cell<Q16>(A, src_plane(A.g, bb ? x : x - cx), bb ? y : y - cy, bb ? z : z - cz, s);
+  const Coef<float> C = coeffs<float, FORCE>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], s[7], s[8], s[9], A.R);
+  float E, O;
+  eval_eo_rt<Q>(C, cx, cy, cz, E, O);
+  add_moments(m, cx, cy, cz, bb ? (E - O) : (E + O));
+}
+
 template <bool Q16, bool FORCE, bool DITHER, int MODE, int Q>
 __global__ void __launch_bounds__(96) pull_list3(const __grid_constant__ StepArgs A,
                                                  const int64_t* __restrict__ cells,
@@ -313,6 +360,14 @@ __global__ void __launch_bounds__(96) pull_list3(const __grid_constant__ StepArg
       y = (int)(r / g.nz);
       z = (int)(r - (int64_t)y * g.nz);
       const uint32_t mask = masks[idx];
+#if HLBM_PULL_RT
+      if (MODE == 0) {
+        (void)mc;
+#pragma unroll 1
+        for (int I = 0; I < Q; ++I)
+          if (kCX[I] == w - 1) pull_link_rt<Q16, FORCE, Q>(A, I, x, y, z, mask, m);
+      } else
+#endif
       if (w == 0) PullGroup<0, -1, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
       else if (w == 1) PullGroup<0, 0, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);
       else PullGroup<0, 1, Q16, FORCE, MODE, Q>::run(A, x, y, z, mask, m, mc);

@@ -20,6 +20,9 @@ namespace hlbm {
 #ifndef HLBM_HALO_WARPS
 #define HLBM_HALO_WARPS 1
 #endif
+#ifndef HLBM_PULL_RT
+#define HLBM_PULL_RT 1
+#endif
 #ifndef HLBM_IDLE_ROWS
 #define HLBM_IDLE_ROWS 1
 #endif
