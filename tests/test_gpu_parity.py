@@ -441,3 +441,29 @@ def test_d3q19_interior_non_default_codecs(quant):
     for kind, w in res.items():
         d = np.abs(codec.unpack(w).astype(np.int64) - codec.unpack(ref).astype(np.int64))
         assert d.max() <= 1, (kind, d.max())
+
+
+@pytest.mark.parametrize("shape", [(6, 1, 64), (6, 2, 64), (8, 16, 64), (6, 31, 72), (10, 47, 40)])
+@pytest.mark.parametrize("dither", [False, True])
+def test_q16_no_stats_path_matches_stats_path_and_oracle(shape, dither):
+    """The no-statistics interior kernels (step_async: the bench's hot path) skip the arithmetic
+    of rows past the first row beyond ny in the last y tile; ny values around the
+    15-row tile cover 1, 2, 16 and 31 rows.  Bitwise equal to the statistics path over 3 steps,
+    1 LSB of the oracle after one."""
+    quant = QuantSpec(dither=dither)
+    state = OS.random_state(shape, seed=5, drho=0.05, umax=0.05, sneq=0.005)
+    w0, _ = codec.encode_state(state[0], state[1], neq_decompose(*state))
+    cfg = SolverConfig(nu=0.02, precision="q16", quant=quant, seed=7)
+    out = {}
+    for path in ("stats", "async"):
+        with Solver(SimGrid(shape), cfg) as s:
+            s.codes = w0
+            for k in range(3):
+                s.step(1) if path == "stats" else s.step_async(1)
+                if k == 0:
+                    out[path + "1"] = s.codes
+            out[path] = s.codes
+    assert np.array_equal(out["stats"], out["async"])
+    ref, _ = OS.fluid_step_q16(w0, cfg.tau, 0, dither=dither, seed=7)
+    d = np.abs(codec.unpack(out["async1"]).astype(np.int64) - codec.unpack(ref).astype(np.int64))
+    assert d.max() <= 1
