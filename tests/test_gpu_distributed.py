@@ -29,6 +29,8 @@ def _config(kind):
     from paper_2602_05295_b200 import QuantSpec, SolverConfig
     if kind == "periodic_q16":
         return SolverConfig(nu=0.02, precision="q16", quant=QuantSpec(dither=True), seed=3)
+    if kind == "periodic_d3q19":
+        return SolverConfig(nu=0.02, precision="q16", quant=QuantSpec(dither=True), seed=3, lattice="D3Q19")
     if kind == "channel_fp32":
         return SolverConfig(nu=0.02, bc={"x": ("inflow", "outflow"), "y": ("periodic", "periodic"),
                                          "z": ("wall", "wall")}, u_in=(0.05, 0, 0))
@@ -41,7 +43,7 @@ def _inputs(kind):
     from oracle import step as OS
     from paper_2602_05295_b200.geometry import sphere_mask
     state = OS.random_state(GDIMS, seed=21, drho=0.04, umax=0.05, sneq=0.004)
-    mask = None if kind == "periodic_q16" else sphere_mask(GDIMS, (19, 11.5, 15.5), 5)
+    mask = None if kind.startswith("periodic") else sphere_mask(GDIMS, (19, 11.5, 15.5), 5)
     return state, mask
 
 
@@ -150,7 +152,7 @@ def test_ipc_peer_store_with_host_jitter():
 
 
 @pytest.mark.parametrize("world,kind", [(2, "periodic_q16"), (3, "periodic_q16"), (3, "channel_q16"),
-                                        (2, "channel_fp32")])
+                                        (2, "channel_fp32"), (2, "periodic_d3q19")])
 def test_distributed_solver_ipc_peer_store_bitwise(world, kind):
     """transport="ipc": CUDA IPC mappings of the neighbours' buffers, edge planes pushed straight
     into their ghost planes, interprocess events between the ranks' streams."""
