@@ -136,3 +136,46 @@ def test_ctypes_layout_matches_the_c_header(tmp_path):
         want.append(f"{cname} size {C.sizeof(st)}")
         want += [f"{cname} {f} {getattr(st, f).offset}" for f, _ in st._fields_]
     assert [g for g in got if g] == want
+
+
+# ---- a plain-C host of the C-ABI (examples/tgv_c.c): the header is C99, the program links
+def _build_c_example(tmp_path):
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "tgv_c"
+    libdir = root / "paper_2602_05295_b200"
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", f"-I{root / 'include'}",
+           str(root / "examples" / "tgv_c.c"), f"-L{libdir}", "-lhlbm", f"-Wl,-rpath,{libdir}", "-lm",
+           "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    assert _build_c_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "q16"])
+def test_c_example_matches_python_host(tmp_path, precision):
+    """The same TGV 32^3 x 10 steps through the C host and through the Python host agree (the
+    inputs are built with C libm and with NumPy, so to rounding of the float64 inputs)."""
+    import subprocess
+    from paper_2602_05295_b200 import SimGrid, Solver, SolverConfig
+    from paper_2602_05295_b200.geometry import taylor_green_fields
+    exe = _build_c_example(tmp_path)
+    out = tmp_path / "rho.bin"
+    r = subprocess.run([str(exe), "32", "10", precision, str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "finite 1" in r.stdout
+    rho_c = np.fromfile(out, dtype=np.float64).reshape(32, 32, 32)
+    with Solver(SimGrid((32, 32, 32)), SolverConfig(nu=0.01, precision=precision)) as s:
+        s.set_equilibrium(*taylor_green_fields(32))
+        s.step(10)
+        rho_py = s.moments()[0]
+    tol = 1e-9 if precision == "fp32" else 2.2e-5      # q16: 2 LSB of rho (0.7 / 65535)
+    assert np.max(np.abs(rho_c - rho_py)) <= tol
