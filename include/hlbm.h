@@ -131,7 +131,7 @@ int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
 int hlbm_fluid_update(hlbm_ctx* ctx, int32_t with_stats);
 int hlbm_solid_correction(hlbm_ctx* ctx, hlbm_stats* out);
 /* the streaming operator S alone (reconstruct the stored moments, pull-stream with the BC and
- * voxel bounce-back rules, extract; no collision): converts an Alg.-1 state (post-collision) to
+ * voxel bounce-back / mesh Eq.-8 rules, extract; no collision): converts an Alg.-1 state (post-collision) to
  * the split scheme's storage cut, (S o C)^n o S = S o (C o S)^n.  Not a time step. */
 int hlbm_stream(hlbm_ctx* ctx);
 /* the same launches, enqueued on the context stream without synchronising */
@@ -149,7 +149,8 @@ int hlbm_step_percell(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
  * tiles + halo), streams from its neighbours there (solid links: bounce-back inline), extracts,
  * collides and writes back.  The in-repo baseline of the split-scheme attribution
  * (PAPER.md:418-429).  Related to hlbm_step by the half-step alignment (S o C)^n o S = S o (C o S)^n
- * (SPEC.md:495).  Voxel solids only, single domain. */
+ * (SPEC.md:495).  Voxel solids, or a triangle mesh (a cut link takes the Eq.-8 population built
+ * from the node's own stored post-collision moments); single domain. */
 int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
 
 /* boundary list: global linear cell indices (sorted) and link masks; cells==NULL -> count only */

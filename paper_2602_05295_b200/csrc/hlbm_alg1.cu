@@ -51,9 +51,51 @@ struct GatherAll<Q, Q> {
   __device__ __forceinline__ static void run(const float*, int, uint32_t, float*) {}
 };
 
-template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE>
+// triangle mesh (Alg. 1's link-intersection test, with the cut links of the
+// static mesh precomputed, hlbm_mesh.cu): a cut link takes the Eq.-8 boundary population at
+// p = x - t c_i built from the node's own post-collision moments -- the stored Alg.-1 state -- as
+// the split scheme's compacted kernel builds it from the post-collision state of x
+// (hlbm_cells.cuh pull_link, MODE 2); links into a wall face bounce back.
+template <int I, int Q>
+struct GatherMesh {
+  __device__ __forceinline__ static void run(const StepArgs& A, const float* f, int own, uint32_t mask,
+                                             uint32_t wmask, const float* tk, int x, int y, int z,
+                                             const MeshCtx& mc, float m[10]) {
+    constexpr int cx = kCX[I], cy = kCY[I], cz = kCZ[I];
+    constexpr int opp = I == 0 ? 0 : ((I & 1) ? I + 1 : I - 1);
+    const bool wc = (wmask >> I) & 1u;
+    const bool cut = ((mask >> I) & 1u) && !wc;
+    float ft = wc ? f[opp * kA1N + own] : f[I * kA1N + own - (cx * kA1H + cy) * kA1H - cz];
+    if (cut) {
+      const float t = tk[I];
+      const float px = (float)x - t * cx, py = (float)y - t * cy, pz = (float)z - t * cz;
+      const float rx = px - A.solid_c[0], ry = py - A.solid_c[1], rz = pz - A.solid_c[2];
+      const float ux = A.solid_v[0] + A.solid_w[1] * rz - A.solid_w[2] * ry;
+      const float uy = A.solid_v[1] + A.solid_w[2] * rx - A.solid_w[0] * rz;
+      const float uz = A.solid_v[2] + A.solid_w[0] * ry - A.solid_w[1] * rx;
+      const float r = mc.rho;
+      const Coef<float> Cp = hermite<float>(mc.d, r * ux, r * uy, r * uz, ux, uy, uz, r * ux * ux + mc.nxx,
+                                            r * ux * uy + mc.nxy, r * ux * uz + mc.nxz, r * uy * uy + mc.nyy,
+                                            r * uy * uz + mc.nyz, r * uz * uz + mc.nzz);
+      float Ep, Op;
+      eval_eo<cx, cy, cz, float, Q>(Cp, Ep, Op);
+      ft = Ep + Op;
+    }
+    add_moments(m, cx, cy, cz, ft);
+    GatherMesh<I + 1, Q>::run(A, f, own, mask, wmask, tk, x, y, z, mc, m);
+  }
+};
+template <int Q>
+struct GatherMesh<Q, Q> {
+  __device__ __forceinline__ static void run(const StepArgs&, const float*, int, uint32_t, uint32_t, const float*,
+                                             int, int, int, const MeshCtx&, float*) {}
+};
+
+template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE, bool MESH>
 __global__ void __launch_bounds__(kA1 * kA1 * kA1, 2) alg1_step(const __grid_constant__ StepArgs A,
-                                                                const uint32_t* __restrict__ fmask) {
+                                                                const uint32_t* __restrict__ fmask,
+                                                                const int32_t* __restrict__ midx,
+                                                                const uint32_t* __restrict__ mmasks) {
   extern __shared__ float fsm[];   // [Q][kA1N]
   const Geo& g = A.g;
   const int tz = (g.nz + kA1 - 1) / kA1, ty = (g.ny + kA1 - 1) / kA1;
@@ -95,7 +137,19 @@ __global__ void __launch_bounds__(kA1 * kA1 * kA1, 2) alg1_step(const __grid_con
 #pragma unroll
       for (int c = 0; c < 10; ++c) m[c] = 0.f;
       const int own = ((lx + 1) * kA1H + (ly + 1)) * kA1H + (lz + 1);
-      GatherAll<0, Q>::run(fsm, own, mask, m);
+      const int k = MESH ? midx[cell] : -1;
+      if (MESH && k >= 0) {
+        float o[10];   // the node's own stored (post-collision) moments
+        load_cell<Q16>(A, x + 1, y, z, o);
+        MeshCtx mc;
+        mc.rho = 1.0f + o[0];
+        mc.d = o[0];
+        mc.nxx = o[4]; mc.nxy = o[5]; mc.nxz = o[6]; mc.nyy = o[7]; mc.nyz = o[8]; mc.nzz = o[9];
+        GatherMesh<0, Q>::run(A, fsm, own, mmasks[k], A.wall_masks ? A.wall_masks[k] : 0u, A.cut_t + (int64_t)k * 27,
+                              x, y, z, mc, m);
+      } else {
+        GatherAll<0, Q>::run(fsm, own, mask, m);
+      }
       float pre[10];
       raw_to_state<float>(m, pre);
       if (!COLLIDE) {   // the streaming operator S alone (hlbm_stream)
@@ -114,35 +168,59 @@ __global__ void __launch_bounds__(kA1 * kA1 * kA1, 2) alg1_step(const __grid_con
   if (A.do_stats) flush_stats(A, red);
 }
 
-template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE>
-static cudaError_t launch_alg1_t(const StepArgs& A, const uint32_t* fmask, cudaStream_t st) {
+template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE, bool MESH>
+static cudaError_t launch_alg1_m(const StepArgs& A, const uint32_t* fmask, const int32_t* midx,
+                                 const uint32_t* mmasks, cudaStream_t st) {
   const Geo& g = A.g;
   const int64_t tiles = (int64_t)((g.nx + kA1 - 1) / kA1) * ((g.ny + kA1 - 1) / kA1) * ((g.nz + kA1 - 1) / kA1);
   const int smem = Q * kA1N * (int)sizeof(float);
   static bool attr = false;   // once per instantiation (not on every launch)
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(alg1_step<Q16, FORCE, DITHER, Q, COLLIDE>,
+    cudaError_t e = cudaFuncSetAttribute(alg1_step<Q16, FORCE, DITHER, Q, COLLIDE, MESH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  alg1_step<Q16, FORCE, DITHER, Q, COLLIDE><<<(unsigned)tiles, kA1 * kA1 * kA1, smem, st>>>(A, fmask);
+  alg1_step<Q16, FORCE, DITHER, Q, COLLIDE, MESH><<<(unsigned)tiles, kA1 * kA1 * kA1, smem, st>>>(A, fmask, midx,
+                                                                                                   mmasks);
+  return cudaGetLastError();
+}
+
+// mesh_idx (dense list positions) selects the triangle-mesh variant (D3Q27 only, like set_mesh)
+template <bool Q16, bool FORCE, bool DITHER, int Q, bool COLLIDE>
+static cudaError_t launch_alg1_t(const StepArgs& A, const uint32_t* fmask, const int32_t* midx,
+                                 const uint32_t* mmasks, cudaStream_t st) {
+  if constexpr (Q == 27) {
+    if (midx) return launch_alg1_m<Q16, FORCE, DITHER, Q, COLLIDE, true>(A, fmask, midx, mmasks, st);
+  }
+  return launch_alg1_m<Q16, FORCE, DITHER, Q, COLLIDE, false>(A, fmask, nullptr, nullptr, st);
+}
+
+__global__ void mesh_index_kernel(const int64_t* __restrict__ cells, int64_t nb, int32_t* __restrict__ out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += (int64_t)gridDim.x * blockDim.x)
+    out[cells[k]] = (int32_t)k;
+}
+
+cudaError_t launch_mesh_index(const int64_t* cells, int64_t nb, int64_t n, int32_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0xFF, (size_t)n * 4, st);   // -1: not listed
+  if (e != cudaSuccess || nb <= 0) return e;
+  mesh_index_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 148 * 8), 256, 0, st>>>(cells, nb, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool force, bool dither, int q,
-                        cudaStream_t st, bool collide) {
+                        cudaStream_t st, bool collide, const int32_t* midx, const uint32_t* mm) {
   if (!collide) {   // S alone: no force term
-    if (q16) return dither ? (q == 19 ? launch_alg1_t<true, false, true, 19, false>(A, fmask, st)
-                                      : launch_alg1_t<true, false, true, 27, false>(A, fmask, st))
-                           : (q == 19 ? launch_alg1_t<true, false, false, 19, false>(A, fmask, st)
-                                      : launch_alg1_t<true, false, false, 27, false>(A, fmask, st));
-    return q == 19 ? launch_alg1_t<false, false, false, 19, false>(A, fmask, st)
-                   : launch_alg1_t<false, false, false, 27, false>(A, fmask, st);
+    if (q16) return dither ? (q == 19 ? launch_alg1_t<true, false, true, 19, false>(A, fmask, midx, mm, st)
+                                      : launch_alg1_t<true, false, true, 27, false>(A, fmask, midx, mm, st))
+                           : (q == 19 ? launch_alg1_t<true, false, false, 19, false>(A, fmask, midx, mm, st)
+                                      : launch_alg1_t<true, false, false, 27, false>(A, fmask, midx, mm, st));
+    return q == 19 ? launch_alg1_t<false, false, false, 19, false>(A, fmask, midx, mm, st)
+                   : launch_alg1_t<false, false, false, 27, false>(A, fmask, midx, mm, st);
   }
 #define HLBM_A1(QQ, F, D)                                                          \
   if (q16 == QQ && force == F && dither == D)                                     \
-    return q == 19 ? launch_alg1_t<QQ, F, D, 19, true>(A, fmask, st) : launch_alg1_t<QQ, F, D, 27, true>(A, fmask, st);
+    return q == 19 ? launch_alg1_t<QQ, F, D, 19, true>(A, fmask, midx, mm, st) : launch_alg1_t<QQ, F, D, 27, true>(A, fmask, midx, mm, st);
   HLBM_A1(false, false, false)
   HLBM_A1(false, true, false)
   HLBM_A1(true, false, false)

@@ -210,7 +210,17 @@ void free_mesh(hlbm_ctx* ctx) {
   cudaFree(ctx->mesh.t32);
   cudaFree(ctx->mesh.tri);
   cudaFree(ctx->mesh.wmasks);
+  cudaFree(ctx->mesh.dense);
   ctx->mesh = MeshLinks();
+}
+
+// dense per-cell positions in the cut-link list for the fused Alg.-1 kernel (built once per mesh)
+int mesh_dense(hlbm_ctx* ctx) {
+  if (!ctx->mesh.nb || ctx->mesh.dense) return HLBM_OK;
+  const int64_t n = (int64_t)ctx->cfg.nx * ctx->cfg.ny * ctx->cfg.nz;
+  CK(cudaMalloc(&ctx->mesh.dense, (size_t)n * 4));
+  CK(launch_mesh_index(ctx->mesh.cells, ctx->mesh.nb, n, ctx->mesh.dense, ctx->stream));
+  return HLBM_OK;
 }
 
 bool has_force(const hlbm_ctx* ctx) {
@@ -1103,10 +1113,11 @@ int hlbm_solid_correction(hlbm_ctx* ctx, hlbm_stats* out) {
 int hlbm_stream(hlbm_ctx* ctx) {
   if (!ctx) return HLBM_EINVAL;
   SETTLE(ctx);
-  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the streaming operator supports voxel solids only");
   if (ctx->cfg.x_lo_remote || ctx->cfg.x_hi_remote) return fail(ctx, HLBM_EINVAL, "single domain only");
+  if (int r = mesh_dense(ctx)) return r;
   StepArgs A = make_args(ctx, 0);
-  CK(launch_alg1(A, ctx->d_fused, ctx->q16, false, ctx->q16 && ctx->cfg.dither, ctx->q, ctx->stream, false));
+  CK(launch_alg1(A, ctx->d_fused, ctx->q16, false, ctx->q16 && ctx->cfg.dither, ctx->q, ctx->stream, false,
+                 ctx->mesh.dense, ctx->mesh.masks));
   ++ctx->launches;
   if (ctx->cfg.ny == 1) CK(launch_fill_ghosts(make_geo(ctx), ctx->NC, ctx->buf[1 - ctx->cur], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1214,9 +1225,9 @@ int hlbm_step_percell(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
 int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
   if (!ctx || nsteps < 0) return fail(ctx, HLBM_EINVAL, "bad arguments");
   SETTLE(ctx);
-  if (ctx->mesh.nb) return fail(ctx, HLBM_EINVAL, "the fused Alg.-1 step supports voxel solids only");
   if (ctx->cfg.x_lo_remote || ctx->cfg.x_hi_remote)
     return fail(ctx, HLBM_EINVAL, "the fused Alg.-1 step runs on a single domain");
+  if (int r = mesh_dense(ctx)) return r;
   const bool q16 = ctx->q16, force = has_force(ctx), dither = q16 && ctx->cfg.dither;
   float tf = 0.f;
   for (int s = 0; s < nsteps; ++s) {
@@ -1224,7 +1235,8 @@ int hlbm_step_fused(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out) {
     if (st) CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     StepArgs A = make_args(ctx, st);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    CK(launch_alg1(A, ctx->d_fused, q16, force, dither, ctx->q, ctx->stream, true));
+    CK(launch_alg1(A, ctx->d_fused, q16, force, dither, ctx->q, ctx->stream, true, ctx->mesh.dense,
+                   ctx->mesh.masks));
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     ++ctx->launches;
     if (ctx->cfg.ny == 1) {   // one-row slab: both ghost rows hold the edge row's image

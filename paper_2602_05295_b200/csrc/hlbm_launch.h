@@ -23,6 +23,7 @@ struct MeshLinks {               // cut-link table of a static triangle mesh (de
   int* tri = nullptr;            // (nb, 27) triangle index, -1 where uncut
   uint32_t* wmasks = nullptr;    // with wall faces: bit i = the link crosses a wall (bounce-back; the
                                  // list is then the union of mesh-cut and wall-adjacent cells)
+  int32_t* dense = nullptr;      // per-cell list position or -1 (built for the fused Alg.-1 step)
   int64_t nb = 0;
 };
 cudaError_t build_mesh_links(const double* dV, const int* dF, int nf, int nx, int ny, int nz, MeshLinks& out,
@@ -45,7 +46,10 @@ cudaError_t launch_pull_cells(const StepArgs& A, const int64_t* cells, const uin
 // original HOME-LBM step (Alg. 1): post-collision storage cut, own-population
 // reconstruction into shared memory, streaming within 8^3 tiles, voxel solid links inline
 cudaError_t launch_alg1(const StepArgs& A, const uint32_t* fmask, bool q16, bool force, bool dither, int q,
-                        cudaStream_t st, bool collide);
+                        cudaStream_t st, bool collide, const int32_t* mesh_idx = nullptr,
+                        const uint32_t* mesh_masks = nullptr);
+// dense per-cell position in the mesh cut-link list (-1: not listed), for the fused step
+cudaError_t launch_mesh_index(const int64_t* cells, int64_t nb, int64_t n, int32_t* out, cudaStream_t st);
 cudaError_t launch_import(const Geo& g, const Ranges& R, bool q16, void* dst, const double* rho,
                           const double* mom, const double* stress, int x0, int cnt,
                           unsigned long long* sat, unsigned int* nonpos, cudaStream_t st);

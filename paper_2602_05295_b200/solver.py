@@ -295,7 +295,8 @@ class Solver:
         read as POST-collision moments (Alg. 1's storage cut); per node reconstruct own f, stream
         through shared memory (8^3 tiles), solid links inline, extract, collide, write back.  n steps
         of it from m0 followed by one streaming S equal n split steps from S(m0).
-        The in-repo baseline of the split scheme (voxel solids, single domain)."""
+        The in-repo baseline of the split scheme (voxel solids or a triangle mesh: cut links take the
+        Eq.-8 population from the node's own stored post-collision moments; single domain)."""
         self.state_version += 1
         s = _lib.HlbmStats()
         self._chk(self._lib.hlbm_step_fused(self._ctx, int(n), C.byref(s)))

@@ -45,7 +45,7 @@ def run(name, dims, cfg, init, mask=None, steps=50, mesh=None):
     ms = timed(s, steps)
     st = s.step(3)              # phase split (events around each kernel) + stats
     fused_ms = None
-    if mesh is None:            # the fused Alg.-1 baseline (one kernel, solid links inline)
+    if True:                    # the fused Alg.-1 baseline (one kernel, solid / cut links inline)
         s.step_fused(1)
         fused_ms = s.step_fused(max(2, steps // 10)).t_fluid_ms
     cells = int(np.prod(dims))
