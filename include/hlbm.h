@@ -120,7 +120,9 @@ int hlbm_init_modes(hlbm_ctx* ctx, double rho0, const double* modes, int32_t nmo
 
 /* fluid_update_step x nsteps: interior kernel over every cell, then the
  * compacted boundary/solid kernel; blocks until done and fills *out (may be NULL). Returns
- * HLBM_EDIVERGED when max|u| >= 0.9 or a non-finite value appeared. */
+ * HLBM_EDIVERGED when max|u| >= 0.9 or a non-finite value appeared; hlbm_last_error
+ * then names the step and the node of largest |u| (non-finite first) of the state the step wrote
+ * (SPEC.md:467), found by a scan that runs only on divergence. */
 int hlbm_step(hlbm_ctx* ctx, int32_t nsteps, hlbm_stats* out);
 /* SPEC's split step as two calls (Alg. 2 / Alg. 3 roles):
  * hlbm_fluid_update runs the interior kernel over every cell (no obstacle logic); with obstacles the

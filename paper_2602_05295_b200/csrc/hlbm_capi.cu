@@ -1280,9 +1280,35 @@ static int stats_from_host(hlbm_ctx* ctx, hlbm_stats* out) {
   s.finite = std::isfinite(s.mass) && std::isfinite(s.momentum[0]) && std::isfinite(s.momentum[1]) &&
              std::isfinite(s.momentum[2]) && std::isfinite(s.max_u);
   if (out) *out = s;
-  if (!s.finite) return fail(ctx, HLBM_EDIVERGED, "non-finite moment detected (solver divergence)");
-  if (s.max_u >= 0.9) return fail(ctx, HLBM_EDIVERGED, "max |u| reached 0.9 (solver divergence)");
-  return HLBM_OK;
+  if (s.finite && s.max_u < 0.9) return HLBM_OK;
+  // divergence ("divergence report with step and node"): locate the node in the state
+  // the step wrote -- a scan that runs only here, never on the hot path
+  std::string where;
+  if (staging(ctx, 8) == HLBM_OK) {
+    unsigned long long key = 0;
+    StepArgs A = make_args(ctx, 0);
+    A.in = ctx->buf[ctx->cur];
+    if (launch_locate(A, ctx->q16, reinterpret_cast<unsigned long long*>(ctx->d_stage), ctx->stream) == cudaSuccess &&
+        cudaMemcpyAsync(&key, ctx->d_stage, 8, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess &&
+        cudaStreamSynchronize(ctx->stream) == cudaSuccess) {
+      const int64_t i = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+      const int64_t yz = (int64_t)c.ny * c.nz;
+      const uint32_t bits = (uint32_t)(key >> 32);
+      float u2;
+      memcpy(&u2, &bits, 4);
+      char buf[160];
+      snprintf(buf, sizeof buf, " at step %lld, node (%lld, %lld, %lld)%s", (long long)s.step,
+               (long long)(c.x0 + i / yz), (long long)((i % yz) / c.nz), (long long)(i % c.nz),
+               bits == 0xFFFFFFFFu ? " (non-finite)" : "");
+      where = buf;
+      if (bits != 0xFFFFFFFFu) {
+        snprintf(buf, sizeof buf, ", |u| = %.4g", std::sqrt((double)u2));
+        where += buf;
+      }
+    }
+  }
+  if (!s.finite) return fail(ctx, HLBM_EDIVERGED, "non-finite moment detected (solver divergence)" + where);
+  return fail(ctx, HLBM_EDIVERGED, "max |u| reached 0.9 (solver divergence)" + where);
 }
 
 int hlbm_read_stats(hlbm_ctx* ctx, hlbm_stats* out) {

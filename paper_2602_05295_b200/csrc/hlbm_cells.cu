@@ -444,4 +444,43 @@ cudaError_t launch_special_bits(const uint8_t* cls, int nx, int ny, int nz, int 
   return cudaGetLastError();
 }
 
+
+// divergence locator (runs only after a step reported divergence): the node of largest |u|^2 in the
+// current state, non-finite moments ranking above every finite value; key = u2 bits << 32 | ~index
+// (ties: the smallest linear index)
+template <bool Q16>
+__global__ void locate_kernel(const __grid_constant__ StepArgs A, unsigned long long* __restrict__ out) {
+  const Geo& g = A.g;
+  const int64_t n = (int64_t)g.nx * g.ny * g.nz;
+  unsigned long long best = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i / ((int64_t)g.ny * g.nz));
+    const int64_t r = i - (int64_t)x * g.ny * g.nz;
+    const int y = (int)(r / g.nz), z = (int)(r - (int64_t)y * g.nz);
+    float s[10];
+    load_cell<Q16>(A, x + 1, y, z, s);
+    bool fin = true;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) fin = fin && isfinite(s[c]);
+    const float rho = 1.0f + s[0];
+    const float u2 = (s[1] * s[1] + s[2] * s[2] + s[3] * s[3]) / (rho * rho);
+    const uint32_t bits = (fin && isfinite(u2)) ? __float_as_uint(fmaxf(u2, 0.f)) : 0xFFFFFFFFu;
+    const unsigned long long key = ((unsigned long long)bits << 32) | (0xFFFFFFFFull - (unsigned long long)(uint32_t)i);
+    best = key > best ? key : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+    best = v > best ? v : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+cudaError_t launch_locate(const StepArgs& A, bool q16, unsigned long long* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, 8, st);
+  if (e != cudaSuccess) return e;
+  if (q16) locate_kernel<true><<<148 * 8, 256, 0, st>>>(A, out);
+  else locate_kernel<false><<<148 * 8, 256, 0, st>>>(A, out);
+  return cudaGetLastError();
+}
 }  // namespace hlbm

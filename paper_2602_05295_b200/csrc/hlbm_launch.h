@@ -67,6 +67,8 @@ cudaError_t launch_compact(const uint8_t* cls, const uint32_t* links, int64_t n,
 cudaError_t launch_special_bits(const uint8_t* cls, int nx, int ny, int nz, int row_words,
                                 uint32_t* bits, cudaStream_t st);
 cudaError_t launch_fill_ghosts(const Geo& g, int NC, void* buf, cudaStream_t st);
+// the node of largest |u|^2 (non-finite first) of the state A.in: key = u2 bits << 32 | ~linear index
+cudaError_t launch_locate(const StepArgs& A, bool q16, unsigned long long* out, cudaStream_t st);
 cudaError_t launch_pack_codes(const Geo& g, int NC, void* buf, uint32_t* dense, int dir, cudaStream_t st);
 cudaError_t launch_init_modes(const Geo& g, bool q16, const Ranges& R, void* dst, double rho0,
                               const double* modes, int nmodes, cudaStream_t st);

@@ -159,6 +159,29 @@ def test_divergence_raises_floating_point_error():
             s.step(1)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "q16"])
+def test_divergence_report_names_step_and_node(precision):
+    """the divergence report carries the step and the node -- here one fast spot in a
+    fluid at rest; the locator scan runs only after a step reported divergence."""
+    shape = (12, 8, 16)
+    rho = np.ones(shape)
+    mom = np.zeros((3,) + shape)
+    blk = (slice(6, 9), slice(2, 5), slice(9, 12))     # a 3^3 block centred on (7, 3, 10): rho 0.8,
+    rho[blk] = 0.8                                     # j = (0.6, 0.6, 0), |u| = 1.06 -- inside the
+    mom[0][blk] = 0.6                                  # 16-bit ranges, so both precisions store it
+    mom[1][blk] = 0.6
+    st = neq_recompose(rho, mom, np.zeros((6,) + shape))
+    with Solver(SimGrid(shape), SolverConfig(nu=0.02, precision=precision)) as s:
+        s.set_moments(rho, mom, st)
+        with pytest.raises(FloatingPointError) as e:
+            s.step(1)
+        msg = str(e.value)
+    print(msg)
+    assert "at step" in msg and "node (" in msg
+    x, y, z = (int(v) for v in msg.split("node (")[1].split(")")[0].split(","))
+    assert abs(x - 7) <= 1 and abs(y - 3) <= 1 and abs(z - 10) <= 1
+
+
 def test_moment_set_accessor():
     state = OS.random_state((8, 8, 8), seed=6, drho=0.05, umax=0.05, sneq=0.005)
     with Solver(SimGrid((8, 8, 8)), SolverConfig(nu=0.02)) as s:
