@@ -223,7 +223,8 @@ class DistributedSolver:
         import torch.distributed as dist
         if not self._cuda or not hasattr(self.solver, "ipc_export"):
             raise ValueError("transport='ipc' needs the CUDA Solver")
-        if not self.overlap or self.plan.nx <= 2:
+        # decided from the full partition, identically on every rank, before any collective
+        if not self.overlap or min(p.nx for p in partition(self.plan.gnx, self.world, False)) <= 2:
             raise ValueError("transport='ipc' needs the overlapped schedule and > 2 planes per rank")
         # host ordering of the interprocess event records (see the module docstring)
         self._hostpg = self.group if dist.get_backend(self.group) == "gloo" else dist.new_group(backend="gloo")

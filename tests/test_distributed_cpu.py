@@ -199,3 +199,12 @@ def test_transport_validation():
         DistributedSolver((8, 4, 4), cfg, rank=0, world=1, solver=object(), transport="ipc")
     with pytest.raises(ValueError, match="transport"):
         DistributedSolver((8, 4, 4), cfg, rank=0, world=1, solver=object(), transport="tcp")
+
+
+def test_ipc_slab_size_check_is_the_same_on_every_rank():
+    """The > 2 planes rule is decided from the whole partition (before any collective), so a rank
+    with enough planes refuses exactly when another rank would (no rank left waiting in a
+    collective).  gnx = 7 over 3 ranks: slabs 3, 2, 2 -> every rank refuses, rank 0 included."""
+    from paper_2602_05295_b200.distributed import partition
+    assert [p.nx for p in partition(7, 3, True)] == [3, 2, 2]
+    assert min(p.nx for p in partition(7, 3, False)) <= 2
