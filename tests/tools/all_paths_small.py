@@ -34,4 +34,7 @@ with Solver(SimGrid(shape), SolverConfig(nu=0.02, precision="q16")) as s:
     s.set_moments(*state)
     s.step(2)
     s.cut_links()
+    s.step_fused(2)      # Alg. 1 with the mesh's cut links
+    s.stream()
+    s.moments()
 print("mesh ok")
