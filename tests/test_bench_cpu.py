@@ -45,6 +45,12 @@ def test_self_launch_spawns_n_ranks_reference_arm():
     import json
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    # the reference arm's contract: same metric / unit / direction as our arm, a cpu_baseline
+    # describing this run, and an e2e object with no host<->device bytes
+    assert d["unit"] == "MLUPS" and d["higher_is_better"] is True and d["metric"].startswith("MLUPS")
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
 def test_xslab_reference_step_equals_periodic_step(tmp_path):
