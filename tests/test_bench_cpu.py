@@ -70,3 +70,31 @@ def test_xslab_reference_step_equals_periodic_step(tmp_path):
     kind, step, _ = bench._ref_modules()
     r, m, s = step(st[0], st[1:4], st[4:10], bench.TAU)
     np.testing.assert_allclose(got, np.concatenate([r[None], m, s]), rtol=0, atol=1e-15)
+
+
+@pytest.mark.gpu
+def test_bench_json_contract_on_gpu():
+    """`bench.py` (our arm, N = 1) prints one JSON line with every key the driver reads."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["BENCH_REF_N"] = "16"
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "5", "--warmup", "3"],
+                         capture_output=True, text=True, env=env, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    import json
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
+    assert d["gpu_launches"] >= d["steps"]
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
+    assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-3
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
+    assert "workload" in d["config"] and "l2" in d["config"]
+    assert d["clocks"]["sm_mhz"] > 0 and isinstance(d["clocks"]["reasons"], list)
